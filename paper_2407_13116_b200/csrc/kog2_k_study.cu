@@ -1,0 +1,400 @@
+// kog2_k_study.cu — the verification path on the device: svd2_ext
+// (oracle.hpp:102-238), the per-matrix error measures (oracle.hpp:267-301),
+// and the fused study kernel generate -> svd2_ext -> svd2 | lasv2 ->
+// finiteness -> metrics -> ErrorStats absorb (harness.hpp:190-222), reduced
+// with warp shuffles, shared memory and order-independent global atomics.
+#include "kog2_common.cuh"
+#include "kog2_ext.cuh"
+#include "kog2_gen.cuh"
+#include "kog2_lasv2.cuh"
+
+using namespace kog2;
+
+namespace {
+
+__device__ __forceinline__ kog_extfloat to_c(const Ext& x) { return kog_extfloat{x.e, x.hi, x.lo}; }
+
+template <class T>
+__global__ void k_svd2_ext(InP<T> in, kog_extsvd* o, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    ExtSvd r;
+    svd2_ext(load_mat(in, i), r);
+    kog_extsvd rec;
+    rec.sigma1 = to_c(r.sigma1);
+    rec.sigma2 = to_c(r.sigma2);
+    rec.u[0] = to_c(r.u.a11);
+    rec.u[1] = to_c(r.u.a12);
+    rec.u[2] = to_c(r.u.a21);
+    rec.u[3] = to_c(r.u.a22);
+    rec.v[0] = to_c(r.v.a11);
+    rec.v[1] = to_c(r.v.a12);
+    rec.v[2] = to_c(r.v.a21);
+    rec.v[3] = to_c(r.v.a22);
+    o[i] = rec;
+  }
+}
+
+// run_one's per-matrix body (harness.hpp:190-222) without the absorb; returns
+// the svd2 flags plus KOG_M_NONFINITE_FACTOR / KOG_M_NAN_METRIC
+template <class T>
+__device__ __forceinline__ uint32_t run_one_kog(const Mat<T>& g, const Opt& o, Metrics& m) {
+  ExtSvd ref;
+  svd2_ext(g, ref);
+  Result<T> r;
+  svd2<T>(g, o, r);
+  uint32_t flags = r.flags;
+  if (!all_finite(r.u) || !all_finite(r.v) || !is_finite(r.sigma1.f) || !is_finite(r.sigma2.f))
+    flags |= KOG_M_NONFINITE_FACTOR;
+  metrics(g, r.u, r.v, ext_from_pair(r.sigma1), ext_from_pair(r.sigma2), ref, m);
+  if (isnan(m.reG) || isnan(m.reS1) || isnan(m.reS2) || isnan(m.reU) || isnan(m.reV)) flags |= KOG_M_NAN_METRIC;
+  return flags;
+}
+
+template <class T>
+__device__ __forceinline__ uint32_t run_one_lasv2(const Mat<T>& g, Metrics& m) {
+  ExtSvd ref;
+  svd2_ext(g, ref);
+  const Lasv2<T> r = lasv2(g.g11, g.g12, g.g22);
+  const Mat<T> u{r.csl, -r.snl, r.snl, r.csl};
+  const Mat<T> v{r.csr, -r.snr, r.snr, r.csr};
+  uint32_t flags = 0;
+  if (!all_finite(u) || !all_finite(v) || !is_finite(r.ssmax) || !is_finite(r.ssmin)) flags |= KOG_M_NONFINITE_FACTOR;
+  metrics(g, u, v, ext_from(r.ssmax), ext_from(r.ssmin), ref, m);
+  if (isnan(m.reG) || isnan(m.reS1) || isnan(m.reS2) || isnan(m.reU) || isnan(m.reV)) flags |= KOG_M_NAN_METRIC;
+  return flags;
+}
+
+template <class T>
+__global__ void k_metrics(InP<T> in, kog_metrics* o, uint64_t n, Opt opt) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    Metrics m;
+    const uint32_t flags = run_one_kog<T>(load_mat(in, i), opt, m);
+    kog_metrics rec;
+    rec.reG = m.reG;
+    rec.reS1 = m.reS1;
+    rec.reS2 = m.reS2;
+    rec.reU = m.reU;
+    rec.reV = m.reV;
+    rec.kappa2 = to_c(m.kappa2);
+    rec.kappa_inf = m.kappa_inf;
+    rec.flags = flags;
+    o[i] = rec;
+  }
+}
+
+// ----------------------------------------------------------------- study
+struct KappaBest {
+  Ext k;
+  unsigned long long idx;
+  bool valid;
+};
+
+// (a, ia) beats (b, ib): larger under ext_cmp; ties go to the lower index,
+// which is the reference's first-occurrence rule under its in-order absorb
+// and block-ordered merge (harness.hpp:92-93, 103, 265-270)
+__device__ __forceinline__ bool kappa_better(const Ext& a, unsigned long long ia, const Ext& b,
+                                             unsigned long long ib, bool bvalid) {
+  if (!bvalid) return true;
+  const int c = ext_cmp(a, b);
+  return c > 0 || (c == 0 && ia < ib);
+}
+
+struct BlockPartial {
+  kog_extfloat k;
+  unsigned long long idx;
+  unsigned valid;
+  unsigned pad;
+};
+
+// the five metrics are +0, positive or +inf on the absorbed path (never -0
+// or NaN: ext_ratio and relerr return literal 0.0, NaN aborts the batch), so
+// their bit patterns order like the values and fmax == unsigned max
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+template <class T, int ROUTINE>
+__global__ void __launch_bounds__(kThreads) k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt,
+                                                    kog_stats* stats, BlockPartial* partial) {
+  __shared__ unsigned cnt[19];
+  __shared__ double red[5][kThreads / 32];
+  __shared__ Ext kred_k[kThreads / 32];
+  __shared__ unsigned long long kred_i[kThreads / 32];
+  __shared__ int kred_v[kThreads / 32];
+  if (threadIdx.x < 19) cnt[threadIdx.x] = 0;
+  __syncthreads();
+
+  double mG = 0.0, mS1 = 0.0, mS2 = 0.0, mU = 0.0, mV = 0.0;
+  KappaBest kb{ext_zero(), 0ull, false};
+  bool kinf = false;
+  unsigned long long fail = ~0ull;
+  const unsigned lane = threadIdx.x & 31u;
+
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const unsigned long long index = index0 + i;
+    const Mat<T> g = generate<T>(c, index);
+    Metrics m;
+    uint32_t flags;
+    if (ROUTINE == KOG_ROUTINE_KOG)
+      flags = run_one_kog<T>(g, opt, m);
+    else
+      flags = run_one_lasv2<T>(g, m);
+    bool ok = true;
+    if (flags & KOG_M_NONFINITE_FACTOR) {
+      ok = false;
+      const unsigned long long key = index * 4ull + KOG_FAIL_NONFINITE;
+      if (key < fail) fail = key;
+    } else if (flags & KOG_M_NAN_METRIC) {
+      ok = false;
+      const unsigned long long key = index * 4ull + KOG_FAIL_NAN_METRIC;
+      if (key < fail) fail = key;
+    }
+    if (ok) {  // ErrorStats::absorb (harness.hpp:84-95)
+      mG = fmax(mG, m.reG);
+      mS1 = fmax(mS1, m.reS1);
+      mS2 = fmax(mS2, m.reS2);
+      mU = fmax(mU, m.reU);
+      mV = fmax(mV, m.reV);
+      if (m.kappa_inf) {
+        kinf = true;
+      } else if (ext_cmp(m.kappa2, kb.k) > 0) {  // kb.k starts at zero like maxKappa2
+        kb.k = m.kappa2;  // a lane's indices increase: first occurrence kept
+        kb.idx = index;
+        kb.valid = true;
+      }
+    }
+    if (ROUTINE == KOG_ROUTINE_KOG) {  // BranchCounts::add (harness.hpp:56-64)
+      const unsigned active = __activemask();
+      const unsigned path = (flags >> KOG_F_PATH_SHIFT) & 7u;
+      const unsigned t2p = (flags >> KOG_F_T2P_SHIFT) & 7u;
+      const int leader = __ffs(active) - 1;
+#pragma unroll
+      for (unsigned k = 0; k < 7; ++k) {
+        const unsigned bt = __ballot_sync(active, ok && t2p == k);
+        const unsigned bp = __ballot_sync(active, ok && path == k);
+        if (static_cast<int>(lane) == leader) {
+          if (bt) atomicAdd(&cnt[k], __popc(bt));
+          if (bp) atomicAdd(&cnt[7 + k], __popc(bp));
+        }
+      }
+      const unsigned b0 = __ballot_sync(active, ok && (flags & KOG_F_TANPSI_INF));
+      const unsigned b1 = __ballot_sync(active, ok && (flags & KOG_F_DIAG_SWAP));
+      const unsigned b2 = __ballot_sync(active, ok && (flags & KOG_F_COMPOSE_MINUS));
+      const unsigned b3 = __ballot_sync(active, ok && (flags & KOG_F_SIGMA_SWAP));
+      const unsigned b4 = __ballot_sync(active, ok && (flags & KOG_F_PRESCALE_INEXACT));
+      if (static_cast<int>(lane) == leader) {
+        if (b0) atomicAdd(&cnt[14], __popc(b0));
+        if (b1) atomicAdd(&cnt[15], __popc(b1));
+        if (b2) atomicAdd(&cnt[16], __popc(b2));
+        if (b3) atomicAdd(&cnt[17], __popc(b3));
+        if (b4) atomicAdd(&cnt[18], __popc(b4));
+      }
+    }
+  }
+
+  // ---- warp reduction (every lane participates)
+  for (int off = 16; off > 0; off >>= 1) {
+    mG = fmax(mG, __shfl_down_sync(0xffffffffu, mG, off));
+    mS1 = fmax(mS1, __shfl_down_sync(0xffffffffu, mS1, off));
+    mS2 = fmax(mS2, __shfl_down_sync(0xffffffffu, mS2, off));
+    mU = fmax(mU, __shfl_down_sync(0xffffffffu, mU, off));
+    mV = fmax(mV, __shfl_down_sync(0xffffffffu, mV, off));
+    const unsigned long long of = __shfl_down_sync(0xffffffffu, fail, off);
+    if (of < fail) fail = of;
+    const int okinf = __shfl_down_sync(0xffffffffu, static_cast<int>(kinf), off);
+    kinf = kinf || okinf != 0;
+    Ext ok;
+    ok.e = __shfl_down_sync(0xffffffffu, kb.k.e, off);
+    ok.hi = __shfl_down_sync(0xffffffffu, kb.k.hi, off);
+    ok.lo = __shfl_down_sync(0xffffffffu, kb.k.lo, off);
+    const unsigned long long oi = __shfl_down_sync(0xffffffffu, kb.idx, off);
+    const bool ov = __shfl_down_sync(0xffffffffu, static_cast<int>(kb.valid), off) != 0;
+    if (ov && kappa_better(ok, oi, kb.k, kb.idx, kb.valid)) {
+      kb.k = ok;
+      kb.idx = oi;
+      kb.valid = true;
+    }
+  }
+  const unsigned warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = mG;
+    red[1][warp] = mS1;
+    red[2][warp] = mS2;
+    red[3][warp] = mU;
+    red[4][warp] = mV;
+    kred_k[warp] = kb.k;
+    kred_i[warp] = kb.idx;
+    kred_v[warp] = kb.valid ? 1 : 0;
+    if (fail != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(&stats->fail_key), fail);
+    if (kinf) atomicExch(reinterpret_cast<unsigned long long*>(&stats->kappa_inf), 1ull);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v[5];
+    for (int k = 0; k < 5; ++k) {
+      v[k] = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) v[k] = fmax(v[k], red[k][w]);
+    }
+    atomic_max_nonneg(&stats->reG, v[0]);
+    atomic_max_nonneg(&stats->reS1, v[1]);
+    atomic_max_nonneg(&stats->reS2, v[2]);
+    atomic_max_nonneg(&stats->reU, v[3]);
+    atomic_max_nonneg(&stats->reV, v[4]);
+    KappaBest best{ext_zero(), 0ull, false};
+    for (int w = 0; w < kThreads / 32; ++w)
+      if (kred_v[w] && kappa_better(kred_k[w], kred_i[w], best.k, best.idx, best.valid)) {
+        best.k = kred_k[w];
+        best.idx = kred_i[w];
+        best.valid = true;
+      }
+    BlockPartial bp;
+    bp.k = to_c(best.k);
+    bp.idx = best.idx;
+    bp.valid = best.valid ? 1u : 0u;
+    bp.pad = 0;
+    partial[blockIdx.x] = bp;
+    if (ROUTINE == KOG_ROUTINE_KOG) {
+      for (int k = 0; k < 7; ++k) {
+        if (cnt[k]) atomicAdd(reinterpret_cast<unsigned long long*>(&stats->t2p[k]), static_cast<unsigned long long>(cnt[k]));
+        if (cnt[7 + k])
+          atomicAdd(reinterpret_cast<unsigned long long*>(&stats->path[k]), static_cast<unsigned long long>(cnt[7 + k]));
+      }
+      unsigned long long* tail = reinterpret_cast<unsigned long long*>(&stats->tanpsi_inf);
+      for (int k = 0; k < 5; ++k)
+        if (cnt[14 + k]) atomicAdd(tail + k, static_cast<unsigned long long>(cnt[14 + k]));
+    }
+  }
+}
+
+// merge the per-block (kappa, index) slots into stats (one block)
+__global__ void k_study_finish(kog_stats* stats, const BlockPartial* partial, int nblocks) {
+  __shared__ Ext sk[kThreads];
+  __shared__ unsigned long long si[kThreads];
+  __shared__ int sv[kThreads];
+  KappaBest best{ext_zero(), 0ull, false};
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+    const BlockPartial p = partial[b];
+    if (!p.valid) continue;
+    const Ext k{p.k.e, p.k.hi, p.k.lo};
+    if (kappa_better(k, p.idx, best.k, best.idx, best.valid)) {
+      best.k = k;
+      best.idx = p.idx;
+      best.valid = true;
+    }
+  }
+  sk[threadIdx.x] = best.k;
+  si[threadIdx.x] = best.idx;
+  sv[threadIdx.x] = best.valid;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < static_cast<int>(blockDim.x); ++t)
+      if (sv[t] && kappa_better(sk[t], si[t], best.k, best.idx, best.valid)) {
+        best.k = sk[t];
+        best.idx = si[t];
+        best.valid = true;
+      }
+    // merge with earlier launches; a zero stored kappa means "none yet"
+    const Ext cur{stats->max_kappa2.e, stats->max_kappa2.hi, stats->max_kappa2.lo};
+    if (best.valid && kappa_better(best.k, best.idx, cur, stats->max_kappa2_index, !ext_is_zero(cur))) {
+      stats->max_kappa2 = to_c(best.k);
+      stats->max_kappa2_index = best.idx;
+    }
+  }
+}
+
+template <class T, class MatC>
+int launch_metrics(const MatC* g, kog_metrics* o, uint64_t n, const kog_options* opt, cudaStream_t st) {
+  if (!mat_ok<T>(g) || !o) return kog2_arg_error("kog_metrics_batch: null argument");
+  if (n == 0) return KOG_OK;
+  k_metrics<T><<<grid_for(n, 128), 128, 0, st>>>(in_of<T>(g), o, n, opt_of(opt));
+  return launched("k_metrics");
+}
+
+template <class T, class MatC>
+int launch_ext(const MatC* g, kog_extsvd* o, uint64_t n, cudaStream_t st) {
+  if (!mat_ok<T>(g) || !o) return kog2_arg_error("kog_svd2_ext_batch: null argument");
+  if (n == 0) return KOG_OK;
+  k_svd2_ext<T><<<grid_for(n, 128), 128, 0, st>>>(in_of<T>(g), o, n);
+  return launched("k_svd2_ext");
+}
+
+}  // namespace
+
+extern "C" {
+
+int kog_svd2_ext_batch_f64(const kog_mat_f64* g, kog_extsvd* out, uint64_t n, void* stream) {
+  return launch_ext<double>(g, out, n, KOG2_ST(stream));
+}
+int kog_svd2_ext_batch_f32(const kog_mat_f32* g, kog_extsvd* out, uint64_t n, void* stream) {
+  return launch_ext<float>(g, out, n, KOG2_ST(stream));
+}
+int kog_metrics_batch_f64(const kog_mat_f64* g, kog_metrics* out, uint64_t n, const kog_options* opt, void* stream) {
+  return launch_metrics<double>(g, out, n, opt, KOG2_ST(stream));
+}
+int kog_metrics_batch_f32(const kog_mat_f32* g, kog_metrics* out, uint64_t n, const kog_options* opt, void* stream) {
+  return launch_metrics<float>(g, out, n, opt, KOG2_ST(stream));
+}
+
+int kog_study_stats_alloc(kog_stats** stats_dev) {
+  if (!stats_dev) return kog2_arg_error("kog_study_stats_alloc: null argument");
+  if (cudaMalloc(reinterpret_cast<void**>(stats_dev), sizeof(kog_stats)) != cudaSuccess)
+    return kog2_cuda_error("cudaMalloc(kog_stats)");
+  return kog_study_stats_reset(*stats_dev, nullptr);
+}
+int kog_study_stats_free(kog_stats* stats_dev) {
+  if (stats_dev) cudaFree(stats_dev);
+  return KOG_OK;
+}
+int kog_study_stats_reset(kog_stats* stats_dev, void* stream) {
+  if (!stats_dev) return kog2_arg_error("kog_study_stats_reset: null argument");
+  kog_stats init;
+  kog_stats_init(&init);
+  if (cudaMemcpyAsync(stats_dev, &init, sizeof init, cudaMemcpyHostToDevice, KOG2_ST(stream)) != cudaSuccess)
+    return kog2_cuda_error("cudaMemcpyAsync(kog_stats)");
+  return cudaStreamSynchronize(KOG2_ST(stream)) == cudaSuccess ? KOG_OK : kog2_cuda_error("cudaStreamSynchronize");
+}
+
+int kog_study_batch(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats_dev, void* stream) {
+  if (!cfg || !stats_dev) return kog2_arg_error("kog_study_batch: null argument");
+  if (kog_validate(cfg) != KOG_OK) return KOG_ERR_ARG;
+  if (n == 0) return KOG_OK;
+  // per-block (kappa, index) slots: a lazily grown per-thread, per-device scratch
+  static thread_local BlockPartial* scratch[64] = {};
+  static thread_local int scratch_blocks[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kog2_cuda_error("cudaGetDevice");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint64_t want = (n + kThreads - 1) / kThreads;
+  const uint64_t cap = static_cast<uint64_t>(sms) * 8ull;
+  if (want > cap) want = cap;
+  const int grid = static_cast<int>(want);
+  if (scratch_blocks[dev] < grid) {
+    if (scratch[dev]) cudaFree(scratch[dev]);
+    scratch[dev] = nullptr;
+    if (cudaMalloc(reinterpret_cast<void**>(&scratch[dev]), sizeof(BlockPartial) * grid) != cudaSuccess)
+      return kog2_cuda_error("cudaMalloc(study scratch)");
+    scratch_blocks[dev] = grid;
+  }
+  const GenCfg g = gen_cfg_of(cfg);
+  const Opt o = opt_of(&cfg->options);
+  cudaStream_t st = KOG2_ST(stream);
+  BlockPartial* part = scratch[dev];
+  if (cfg->single_precision) {
+    if (cfg->routine == KOG_ROUTINE_LASV2)
+      k_study<float, KOG_ROUTINE_LASV2><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, part);
+    else
+      k_study<float, KOG_ROUTINE_KOG><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, part);
+  } else {
+    if (cfg->routine == KOG_ROUTINE_LASV2)
+      k_study<double, KOG_ROUTINE_LASV2><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, part);
+    else
+      k_study<double, KOG_ROUTINE_KOG><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, part);
+  }
+  const int rc = launched("k_study");
+  if (rc != KOG_OK) return rc;
+  k_study_finish<<<1, kThreads, 0, st>>>(stats_dev, part, grid);
+  return launched("k_study_finish");
+}
+
+}  // extern "C"

@@ -1,0 +1,389 @@
+// kog2_k_units.cu — batched per-routine entry points (fpcore, epair,
+// classify, svd2 phases, lasv2), the generator and the FP64 probe.  Each
+// kernel is the per-matrix reference routine (cited in include/kog2.h) over
+// one thread per element.
+#include "kog2_common.cuh"
+#include "kog2_gen.cuh"
+#include "kog2_lasv2.cuh"
+
+using namespace kog2;
+
+namespace {
+
+template <class T>
+__global__ void k_hypot(const T* a, const T* b, T* o, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) o[i] = hypot_cr(a[i], b[i]);
+}
+template <class T>
+__global__ void k_split(const T* x, int64_t* e, T* f, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const Split<T> s = split(x[i]);
+    e[i] = s.e;
+    f[i] = s.f;
+  }
+}
+template <class T>
+__global__ void k_assemble(const int64_t* e, const T* f, T* o, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) o[i] = assemble(static_cast<long long>(e[i]), f[i]);
+}
+template <class T>
+__global__ void k_tan2(const T* t, T* o, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) o[i] = tan_from_double_angle(t[i]);
+}
+template <class T>
+__global__ void k_sec(const T* t, T* o, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) o[i] = sec_from_tan(t[i]);
+}
+
+template <class T>
+__global__ void k_epair(int op, const int64_t* xe, const T* xf, const int64_t* ye, const T* yf,
+                        int64_t* oe, T* of, uint8_t* st, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    unsigned err = 0;
+    const long long xee = xe ? xe[i] : 0, yee = ye ? ye[i] : 0;
+    const T xff = xf[i], yff = yf ? yf[i] : T(0);
+    EPair<T> r = ep_zero<T>();
+    bool value_out = false;
+    T val = T(0);
+    switch (op) {
+      case KOG_EPAIR_OPLUS: r = oplus(xff, yff, err); break;
+      case KOG_EPAIR_OMINUS: r = ominus(xff, yff, err); break;
+      case KOG_EPAIR_MUL: r = ep_mul(ep_make<T>(xee, xff, err), ep_make<T>(yee, yff, err), err); break;
+      case KOG_EPAIR_DIV: r = ep_div(ep_make<T>(xee, xff, err), ep_make<T>(yee, yff, err), err); break;
+      case KOG_EPAIR_LESS:
+        value_out = true;
+        val = ep_less(ep_make<T>(xee, xff, err), ep_make<T>(yee, yff, err)) ? T(1) : T(0);
+        break;
+      case KOG_EPAIR_RECIP: r = ep_recip(ep_make<T>(xee, xff, err), err); break;
+      default: r = ep_make<T>(xee, xff, err); break;
+    }
+    if (err) {  // the reference throws std::domain_error: report, zero the outputs
+      st[i] = 1;
+      oe[i] = 0;
+      of[i] = T(0);
+    } else {
+      st[i] = 0;
+      oe[i] = value_out ? 0 : r.e;
+      of[i] = value_out ? val : r.f;
+    }
+  }
+}
+
+template <class T>
+__global__ void k_classify(InP<T> in, kog_classify_out o, T* p11, T* p12, T* p21, T* p22, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const Mat<T> g = load_mat(in, i);
+    unsigned err = 0;
+    const TypeInfo info = classify(g, err);
+    o.status[i] = err ? 1 : 0;
+    if (err) continue;
+    o.t[i] = static_cast<uint8_t>(info.t);
+    o.s_type[i] = info.s_type;
+    o.s[i] = info.s;
+    o.e_G[i] = info.e_G;
+    bool inexact;
+    const Mat<T> gp = prescale(g, info.s, inexact);
+    o.inexact_underflow[i] = inexact;
+    p11[i] = gp.g11;
+    p12[i] = gp.g12;
+    p21[i] = gp.g21;
+    p22[i] = gp.g22;
+  }
+}
+
+template <class T, class Rec>
+__global__ void k_urv15(InP<T> in, Rec* o, uint64_t n, Opt opt) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const Urv15<T> u = urv15<T>(load_mat(in, i), opt);
+    Rec r;
+    r.gppp[0] = u.gppp.g11;
+    r.gppp[1] = u.gppp.g12;
+    r.gppp[2] = u.gppp.g21;
+    r.gppp[3] = u.gppp.g22;
+    r.tan_theta = u.tan_theta;
+    r.sec_theta = u.sec_theta;
+    r.r11 = u.r11;
+    r.r12_raw = u.r12_raw;
+    r.r22_raw = u.r22_raw;
+    r.r[0] = u.r.g11;
+    r.r[1] = u.r.g12;
+    r.r[2] = u.r.g21;
+    r.r[3] = u.r.g22;
+    r.sr0 = u.sr0;
+    r.sr1 = u.sr1;
+    r.s12 = u.s12;
+    r.s22 = u.s22;
+    r.col_swap = u.col_swap;
+    r.row_swap = u.row_swap;
+    r.ext_is_r22 = u.ext_is_r22;
+    r.next = static_cast<uint8_t>(u.next);
+    o[i] = r;
+  }
+}
+
+template <class T, class Rec>
+__global__ void k_trisvd(const T* a, const T* b, const T* c, const uint8_t* t13, Rec* o, uint64_t n, Opt opt) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    unsigned err = 0;
+    const TriSvd<T> ts = tri_svd<T>(a[i], b[i], c[i], t13[i] != 0, opt, err);
+    Rec r;
+    r.tan_phi = ts.tan_phi;
+    r.sec_phi = ts.sec_phi;
+    r.cos_phi = ts.cos_phi;
+    r.sin_phi = ts.sin_phi;
+    r.tan_psi = ts.tan_psi;
+    r.sec_psi = ts.sec_psi;
+    r.cos_psi = ts.cos_psi;
+    r.sin_psi = ts.sin_psi;
+    r.sig1_f = ts.sig1.f;
+    r.sig2_f = ts.sig2.f;
+    r.t2f = ts.t2f;
+    r.sig1_e = ts.sig1.e;
+    r.sig2_e = ts.sig2.e;
+    r.sigma_swapped = ts.sigma_swapped;
+    r.tanpsi_inf = ts.tanpsi_inf;
+    r.t2p = static_cast<uint8_t>(ts.t2p);
+    r.status = err ? 1 : 0;
+    o[i] = r;
+  }
+}
+
+template <class T>
+__global__ void k_compose(const T* tp, const T* tt, const uint8_t* m, T* c, T* s, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    T rc, rs;
+    compose_left(tp[i], tt[i], m[i] != 0, rc, rs);
+    c[i] = rc;
+    s[i] = rs;
+  }
+}
+
+__device__ __forceinline__ void sp_store(int8_t* p, const SP& s) {
+  p[0] = static_cast<int8_t>(s.m00);
+  p[1] = static_cast<int8_t>(s.m01);
+  p[2] = static_cast<int8_t>(s.m10);
+  p[3] = static_cast<int8_t>(s.m11);
+}
+
+template <class T>
+__global__ void k_tri13(InP<T> in, const uint8_t* t, T* r11, T* r12, T* r21, T* r22, int8_t* up,
+                        int8_t* vp, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const Tri13<T> f = triangularize13(load_mat(in, i), t[i]);
+    r11[i] = f.r.g11;
+    r12[i] = f.r.g12;
+    r21[i] = f.r.g21;
+    r22[i] = f.r.g22;
+    sp_store(up + 4 * i, f.uplus);
+    sp_store(vp + 4 * i, f.vplus);
+  }
+}
+
+template <class T>
+__global__ void k_lasv2(const T* f, const T* g, const T* h, T* o6, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const Lasv2<T> r = lasv2(f[i], g[i], h[i]);
+    T* o = o6 + 6 * i;
+    o[0] = r.ssmin;
+    o[1] = r.ssmax;
+    o[2] = r.snr;
+    o[3] = r.csr;
+    o[4] = r.snl;
+    o[5] = r.csl;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_generate(GenCfg c, uint64_t index0, T* o11, T* o12,
+                                                       T* o21, T* o22, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const Mat<T> g = generate<T>(c, index0 + i);
+    st_cs(o11 + i, g.g11);
+    st_cs(o12 + i, g.g12);
+    st_cs(o21 + i, g.g21);
+    st_cs(o22 + i, g.g22);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_fp64_probe(double* sink, uint64_t n, uint32_t iters) {
+  const uint64_t i = gtid();
+  if (i >= n) return;
+  double a0 = 1.0 + 1e-9 * static_cast<double>(i & 1023), a1 = a0 + 0.5, a2 = a0 + 0.25, a3 = a0 + 0.125;
+  double a4 = a0 + 0.0625, a5 = a0 + 0.03125, a6 = a0 + 0.015625, a7 = a0 + 0.0078125;
+  const double m = 0.999999999, c = 1e-12;
+  for (uint32_t k = 0; k < iters; ++k) {
+    a0 = fma(a0, m, c);
+    a1 = fma(a1, m, c);
+    a2 = fma(a2, m, c);
+    a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c);
+    a5 = fma(a5, m, c);
+    a6 = fma(a6, m, c);
+    a7 = fma(a7, m, c);
+  }
+  sink[i] = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+}
+
+template <class T, class MatC>
+int launch_generate(const kog_run_config* cfg, uint64_t index0, const MatC* out, uint64_t n, cudaStream_t st) {
+  if (!cfg || !mat_ok<T>(out)) return kog2_arg_error("kog_generate_batch: null argument");
+  if (kog_validate(cfg) != KOG_OK) return KOG_ERR_ARG;
+  if (n == 0) return KOG_OK;
+  k_generate<T><<<grid_for(n), kThreads, 0, st>>>(gen_cfg_of(cfg), index0, out->g11, out->g12, out->g21,
+                                                   out->g22, n);
+  return launched("k_generate");
+}
+
+}  // namespace
+
+// ===================================================================== C-ABI
+#define KOG_LAUNCH(NAME, KERNEL, ...)                                    \
+  if (n == 0) return KOG_OK;                                             \
+  KERNEL<<<grid_for(n), kThreads, 0, KOG2_ST(stream)>>>(__VA_ARGS__, n); \
+  return launched(NAME);
+
+extern "C" {
+
+int kog_hypot_batch_f64(const double* a, const double* b, double* out, uint64_t n, void* stream) {
+  if (!a || !b || !out) return kog2_arg_error("kog_hypot_batch: null argument");
+  KOG_LAUNCH("k_hypot", k_hypot<double>, a, b, out)
+}
+int kog_hypot_batch_f32(const float* a, const float* b, float* out, uint64_t n, void* stream) {
+  if (!a || !b || !out) return kog2_arg_error("kog_hypot_batch: null argument");
+  KOG_LAUNCH("k_hypot", k_hypot<float>, a, b, out)
+}
+int kog_split_batch_f64(const double* x, int64_t* e, double* f, uint64_t n, void* stream) {
+  if (!x || !e || !f) return kog2_arg_error("kog_split_batch: null argument");
+  KOG_LAUNCH("k_split", k_split<double>, x, e, f)
+}
+int kog_split_batch_f32(const float* x, int64_t* e, float* f, uint64_t n, void* stream) {
+  if (!x || !e || !f) return kog2_arg_error("kog_split_batch: null argument");
+  KOG_LAUNCH("k_split", k_split<float>, x, e, f)
+}
+int kog_assemble_batch_f64(const int64_t* e, const double* f, double* out, uint64_t n, void* stream) {
+  if (!e || !f || !out) return kog2_arg_error("kog_assemble_batch: null argument");
+  KOG_LAUNCH("k_assemble", k_assemble<double>, e, f, out)
+}
+int kog_assemble_batch_f32(const int64_t* e, const float* f, float* out, uint64_t n, void* stream) {
+  if (!e || !f || !out) return kog2_arg_error("kog_assemble_batch: null argument");
+  KOG_LAUNCH("k_assemble", k_assemble<float>, e, f, out)
+}
+int kog_tan_from_double_angle_batch_f64(const double* t2, double* out, uint64_t n, void* stream) {
+  if (!t2 || !out) return kog2_arg_error("kog_tan_from_double_angle_batch: null argument");
+  KOG_LAUNCH("k_tan2", k_tan2<double>, t2, out)
+}
+int kog_tan_from_double_angle_batch_f32(const float* t2, float* out, uint64_t n, void* stream) {
+  if (!t2 || !out) return kog2_arg_error("kog_tan_from_double_angle_batch: null argument");
+  KOG_LAUNCH("k_tan2", k_tan2<float>, t2, out)
+}
+int kog_sec_from_tan_batch_f64(const double* t, double* out, uint64_t n, void* stream) {
+  if (!t || !out) return kog2_arg_error("kog_sec_from_tan_batch: null argument");
+  KOG_LAUNCH("k_sec", k_sec<double>, t, out)
+}
+int kog_sec_from_tan_batch_f32(const float* t, float* out, uint64_t n, void* stream) {
+  if (!t || !out) return kog2_arg_error("kog_sec_from_tan_batch: null argument");
+  KOG_LAUNCH("k_sec", k_sec<float>, t, out)
+}
+
+int kog_epair_batch_f64(int op, const int64_t* xe, const double* xf, const int64_t* ye, const double* yf,
+                        int64_t* out_e, double* out_f, uint8_t* status, uint64_t n, void* stream) {
+  if (!xf || !out_e || !out_f || !status || op < 0 || op > KOG_EPAIR_MAKE)
+    return kog2_arg_error("kog_epair_batch: bad argument");
+  KOG_LAUNCH("k_epair", k_epair<double>, op, xe, xf, ye, yf, out_e, out_f, status)
+}
+int kog_epair_batch_f32(int op, const int64_t* xe, const float* xf, const int64_t* ye, const float* yf,
+                        int64_t* out_e, float* out_f, uint8_t* status, uint64_t n, void* stream) {
+  if (!xf || !out_e || !out_f || !status || op < 0 || op > KOG_EPAIR_MAKE)
+    return kog2_arg_error("kog_epair_batch: bad argument");
+  KOG_LAUNCH("k_epair", k_epair<float>, op, xe, xf, ye, yf, out_e, out_f, status)
+}
+
+int kog_classify_prescale_batch_f64(const kog_mat_f64* in, const kog_classify_out* out, const kog_mat_f64* gp,
+                                    uint64_t n, void* stream) {
+  if (!mat_ok<double>(in) || !out || !mat_ok<double>(gp))
+    return kog2_arg_error("kog_classify_prescale_batch: null argument");
+  KOG_LAUNCH("k_classify", k_classify<double>, in_of<double>(in), *out, gp->g11, gp->g12, gp->g21, gp->g22)
+}
+int kog_classify_prescale_batch_f32(const kog_mat_f32* in, const kog_classify_out* out, const kog_mat_f32* gp,
+                                    uint64_t n, void* stream) {
+  if (!mat_ok<float>(in) || !out || !mat_ok<float>(gp))
+    return kog2_arg_error("kog_classify_prescale_batch: null argument");
+  KOG_LAUNCH("k_classify", k_classify<float>, in_of<float>(in), *out, gp->g11, gp->g12, gp->g21, gp->g22)
+}
+
+int kog_urv15_batch_f64(const kog_mat_f64* gp, kog_urv15_f64* out, uint64_t n, const kog_options* opt,
+                        void* stream) {
+  if (!mat_ok<double>(gp) || !out) return kog2_arg_error("kog_urv15_batch: null argument");
+  if (n == 0) return KOG_OK;
+  k_urv15<double, kog_urv15_f64><<<grid_for(n), kThreads, 0, KOG2_ST(stream)>>>(in_of<double>(gp), out, n, opt_of(opt));
+  return launched("k_urv15");
+}
+int kog_urv15_batch_f32(const kog_mat_f32* gp, kog_urv15_f32* out, uint64_t n, const kog_options* opt,
+                        void* stream) {
+  if (!mat_ok<float>(gp) || !out) return kog2_arg_error("kog_urv15_batch: null argument");
+  if (n == 0) return KOG_OK;
+  k_urv15<float, kog_urv15_f32><<<grid_for(n), kThreads, 0, KOG2_ST(stream)>>>(in_of<float>(gp), out, n, opt_of(opt));
+  return launched("k_urv15");
+}
+int kog_tri_svd_batch_f64(const double* r11, const double* r12, const double* r22, const uint8_t* t13,
+                          kog_trisvd_f64* out, uint64_t n, const kog_options* opt, void* stream) {
+  if (!r11 || !r12 || !r22 || !t13 || !out) return kog2_arg_error("kog_tri_svd_batch: null argument");
+  if (n == 0) return KOG_OK;
+  k_trisvd<double, kog_trisvd_f64><<<grid_for(n), kThreads, 0, KOG2_ST(stream)>>>(r11, r12, r22, t13, out, n, opt_of(opt));
+  return launched("k_trisvd");
+}
+int kog_tri_svd_batch_f32(const float* r11, const float* r12, const float* r22, const uint8_t* t13,
+                          kog_trisvd_f32* out, uint64_t n, const kog_options* opt, void* stream) {
+  if (!r11 || !r12 || !r22 || !t13 || !out) return kog2_arg_error("kog_tri_svd_batch: null argument");
+  if (n == 0) return KOG_OK;
+  k_trisvd<float, kog_trisvd_f32><<<grid_for(n), kThreads, 0, KOG2_ST(stream)>>>(r11, r12, r22, t13, out, n, opt_of(opt));
+  return launched("k_trisvd");
+}
+int kog_compose_left_batch_f64(const double* tp, const double* tt, const uint8_t* m, double* c, double* s,
+                               uint64_t n, void* stream) {
+  if (!tp || !tt || !m || !c || !s) return kog2_arg_error("kog_compose_left_batch: null argument");
+  KOG_LAUNCH("k_compose", k_compose<double>, tp, tt, m, c, s)
+}
+int kog_compose_left_batch_f32(const float* tp, const float* tt, const uint8_t* m, float* c, float* s,
+                               uint64_t n, void* stream) {
+  if (!tp || !tt || !m || !c || !s) return kog2_arg_error("kog_compose_left_batch: null argument");
+  KOG_LAUNCH("k_compose", k_compose<float>, tp, tt, m, c, s)
+}
+int kog_triangularize13_batch_f64(const kog_mat_f64* gp, const uint8_t* t, const kog_mat_f64* r, int8_t* uplus,
+                                  int8_t* vplus, uint64_t n, void* stream) {
+  if (!mat_ok<double>(gp) || !t || !mat_ok<double>(r) || !uplus || !vplus)
+    return kog2_arg_error("kog_triangularize13_batch: null argument");
+  KOG_LAUNCH("k_tri13", k_tri13<double>, in_of<double>(gp), t, r->g11, r->g12, r->g21, r->g22, uplus, vplus)
+}
+int kog_triangularize13_batch_f32(const kog_mat_f32* gp, const uint8_t* t, const kog_mat_f32* r, int8_t* uplus,
+                                  int8_t* vplus, uint64_t n, void* stream) {
+  if (!mat_ok<float>(gp) || !t || !mat_ok<float>(r) || !uplus || !vplus)
+    return kog2_arg_error("kog_triangularize13_batch: null argument");
+  KOG_LAUNCH("k_tri13", k_tri13<float>, in_of<float>(gp), t, r->g11, r->g12, r->g21, r->g22, uplus, vplus)
+}
+int kog_lasv2_batch_f64(const double* f, const double* g, const double* h, double* out6, uint64_t n, void* stream) {
+  if (!f || !g || !h || !out6) return kog2_arg_error("kog_lasv2_batch: null argument");
+  KOG_LAUNCH("k_lasv2", k_lasv2<double>, f, g, h, out6)
+}
+int kog_lasv2_batch_f32(const float* f, const float* g, const float* h, float* out6, uint64_t n, void* stream) {
+  if (!f || !g || !h || !out6) return kog2_arg_error("kog_lasv2_batch: null argument");
+  KOG_LAUNCH("k_lasv2", k_lasv2<float>, f, g, h, out6)
+}
+
+int kog_generate_batch_f64(const kog_run_config* cfg, uint64_t index0, const kog_mat_f64* out, uint64_t n,
+                           void* stream) {
+  return launch_generate<double>(cfg, index0, out, n, KOG2_ST(stream));
+}
+int kog_generate_batch_f32(const kog_run_config* cfg, uint64_t index0, const kog_mat_f32* out, uint64_t n,
+                           void* stream) {
+  return launch_generate<float>(cfg, index0, out, n, KOG2_ST(stream));
+}
+
+int kog_fp64_probe(double* sink, uint64_t threads, uint32_t iters, void* stream) {
+  if (!sink || threads == 0) return kog2_arg_error("kog_fp64_probe: bad argument");
+  const uint64_t blocks = (threads + kThreads - 1) / kThreads;
+  k_fp64_probe<<<static_cast<unsigned>(blocks), kThreads, 0, KOG2_ST(stream)>>>(sink, threads, iters);
+  return launched("k_fp64_probe");
+}
+
+}  // extern "C"

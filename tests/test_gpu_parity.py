@@ -1,0 +1,460 @@
+"""CUDA path vs the oracle: bit-exact parity through the C-ABI (libkog2.so).
+
+The oracle here is the reference itself (oracle/_ref/libkogref.so, compiled
+from the unmodified headers) and, where the two are interchangeable, the
+plain-C restatement.  Every comparison is on bit patterns (signed zeros
+included).  Mirrors the reference's suites: fpcore_test.cpp (hypot vs exact,
+ties, edges), svd2_test.cpp (phases, options), oracle_test.cpp, harness_test.cpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import refbind
+from paper_2407_13116_b200 import capi, configs
+from paper_2407_13116_b200 import kogsvd2 as K
+from tests import _gen
+
+pytestmark = pytest.mark.gpu
+
+DTS = [np.float64, np.float32]
+TDT = {np.float64: torch.float64, np.float32: torch.float32}
+
+
+def dev(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+def compare_svd(got: dict, want: dict, what: str) -> None:
+    """Bit-exact on every field; where the reference threw (non-finite input,
+    KOG_F_DOMAIN_ERROR) only the error bit itself is compared."""
+    gf = (host(got["flags"]) if isinstance(got["flags"], torch.Tensor) else got["flags"]).view(np.uint32)
+    err = (want["flags"] & np.uint32(capi.F_DOMAIN_ERROR)) != 0
+    assert ((gf & np.uint32(capi.F_DOMAIN_ERROR)) != 0).tolist() == err.tolist(), f"{what}: domain-error bits"
+    ok = ~err
+    for k in refbind.OUT_DTYPES:
+        g = host(got[k]) if isinstance(got[k], torch.Tensor) else got[k]
+        if k == "flags":
+            g = g.view(np.uint32)
+        _gen.assert_bits_equal(g[ok], want[k][ok], f"{what}.{k}")
+
+
+def records_equal(got, want, what: str) -> None:
+    """Field-by-field byte equality of two ctypes record arrays (padding ignored)."""
+    rt = type(got[0])
+    for name, ft in rt._fields_:
+        off, size = getattr(rt, name).offset, C.sizeof(ft)
+        gb = np.frombuffer(bytes(got), np.uint8).reshape(len(got), -1)[:, off:off + size]
+        wb = np.frombuffer(bytes(want), np.uint8).reshape(len(want), -1)[:, off:off + size]
+        bad = np.nonzero((gb != wb).any(axis=1))[0]
+        assert bad.size == 0, f"{what}.{name}: {bad.size} records differ, first {bad[0]}"
+
+
+ALL_OPTIONS = [capi.kog_options(h, o, w, 0) for h in (1, 0) for o in (0, 1) for w in (0, 1)]
+
+
+def K_opt(o: capi.kog_options) -> K.Options:
+    return K.Options(bool(o.hypot_is_cr), bool(o.ominus_for_d), int(o.wide_channel))
+
+
+# ------------------------------------------------------------ fpcore
+@pytest.mark.parametrize("dt", DTS)
+def test_hypot_matches_reference_and_exact(cuda, ref, dt):
+    """fpcore_test.cpp:40-50 (10^6 any_finite pairs vs the exact reference)."""
+    n = 1_000_000
+    a = _gen.any_finite(dt, 0x68790001, n, 0)
+    b = _gen.any_finite(dt, 0x68790001, n, 1)
+    got = host(K.hypot_cr(dev(a), dev(b)))
+    want = np.empty_like(a)
+    (ref.hypot_f64 if dt == np.float64 else ref.hypot_f32)(a.ctypes.data, b.ctypes.data, want.ctypes.data, n)
+    _gen.assert_bits_equal(got, want, "hypot vs reference")
+    ex = np.array([_gen.hypot_exact(x, y, dt) for x, y in zip(a[:20000], b[:20000])], dtype=dt)
+    _gen.assert_bits_equal(got[:20000], ex, "hypot vs exact integer reference")
+
+
+@pytest.mark.parametrize("dt", DTS)
+def test_hypot_exact_ties(cuda, dt):
+    """fpcore_test.cpp:53-73: scaled 3-4-5 triples whose hypotenuse is a midpoint."""
+    p = 53 if dt == np.float64 else 24
+    lo, hi = (1 << p) // 5 + 1, ((1 << (p + 1)) - 1) // 5
+    rng = np.random.default_rng(0x68790002)
+    q = rng.integers(lo, hi + 1, size=20000, dtype=np.int64) | 1
+    q = q[(5 * q >= (1 << p)) & (5 * q < (1 << (p + 1)))]
+    x = rng.integers(-40, 41, size=q.size)
+    a = np.ldexp((3 * q).astype(np.float64), x).astype(dt)
+    b = np.ldexp((4 * q).astype(np.float64), x).astype(dt)
+    got = host(K.hypot_cr(dev(a), dev(b)))
+    ex = np.array([_gen.hypot_exact(u, v, dt) for u, v in zip(a, b)], dtype=dt)
+    assert q.size > 1000
+    _gen.assert_bits_equal(got, ex, "hypot ties")
+
+
+@pytest.mark.parametrize("dt", DTS)
+def test_hypot_adversarial_edges(cuda, ref, dt):
+    """fpcore_test.cpp:75-89 plus inf/NaN conventions (fpcore.hpp:142-143)."""
+    fi = np.finfo(dt)
+    mc, mu, nu = fi.smallest_subnormal, fi.tiny, fi.max
+    edge = np.array([0, mc, 2 * mc, mu, mu / 2, 1, 1 + fi.eps, nu, nu / 2, nu / 4, np.sqrt(nu), np.sqrt(mu),
+                     3, 4, 0.5, 1.5], dtype=dt)
+    e = np.concatenate([edge, -edge])
+    a, b = np.meshgrid(e, e)
+    a, b = a.ravel().astype(dt), b.ravel().astype(dt)
+    got = host(K.hypot_cr(dev(a), dev(b)))
+    want = np.empty_like(a)
+    (ref.hypot_f64 if dt == np.float64 else ref.hypot_f32)(a.ctypes.data, b.ctypes.data, want.ctypes.data, a.size)
+    _gen.assert_bits_equal(got, want, "hypot edges")
+    sp = np.array([np.inf, -np.inf, np.nan, 1.0, np.nan], dtype=dt)
+    sq = np.array([2.0, 1.0, 1.0, -np.inf, -np.inf], dtype=dt)
+    g2 = host(K.hypot_cr(dev(sp), dev(sq)))
+    assert np.isinf(g2[0]) and np.isinf(g2[1]) and np.isnan(g2[2]) and np.isinf(g2[3]) and np.isinf(g2[4])
+    assert float(host(K.hypot_cr(dev(np.array([nu], dt)), dev(np.array([1], dt))))[0]) == float(nu)
+
+
+@pytest.mark.parametrize("dt", DTS)
+def test_split_assemble_tan_sec(cuda, ref, dt):
+    """fpcore_test.cpp:115-213 surfaces, bit-exact against the reference."""
+    n = 300_000
+    x = _gen.any_finite(dt, 0x68790005, n)
+    x[:6] = np.array([0, -0.0, np.inf, -np.inf, np.nan, 1.5], dtype=dt)
+    e, f = K.split(dev(x))
+    we, wf = np.empty(n, np.int64), np.empty_like(x)
+    (ref.split_f64 if dt == np.float64 else ref.split_f32)(x.ctypes.data, we.ctypes.data, wf.ctypes.data, n)
+    assert (host(e) == we).all()
+    _gen.assert_bits_equal(host(f)[6:], wf[6:], "split.f")
+    ee = (np.arange(n, dtype=np.int64) % 4000) - 2000
+    ee[:4] = [-200000, 200000, -1100, 1100]
+    got = host(K.assemble(dev(ee), dev(wf)))
+    want = np.empty_like(x)
+    (ref.assemble_f64 if dt == np.float64 else ref.assemble_f32)(ee.ctypes.data, wf.ctypes.data, want.ctypes.data, n)
+    _gen.assert_bits_equal(got[6:], want[6:], "assemble")
+    t = _gen.any_finite(dt, 0x68790006, n)
+    t[:4] = np.array([np.inf, -np.inf, 0, 4 / 3], dtype=dt)
+    for name, fn, rf in (("tan2", K.tan_from_double_angle, "tan2"), ("sec", K.sec_from_tan, "sec")):
+        got = host(fn(dev(t)))
+        want = np.empty_like(t)
+        getattr(ref, f"{rf}_{'f64' if dt == np.float64 else 'f32'}")(t.ctypes.data, want.ctypes.data, n)
+        _gen.assert_bits_equal(got, want, name)
+
+
+@pytest.mark.parametrize("dt", DTS)
+def test_epair_ops(cuda, ref, dt):
+    """epair_test.cpp: every EPair operation incl. the throwing cases."""
+    p, emax, emin = _gen.FMT[dt]
+    n = 200_000
+    x = _gen.positive(dt, 0x45500002, n, emin - p + 1, emax, 0)
+    y = _gen.positive(dt, 0x45500002, n, emin - p + 1, emax, 1)
+    y[::97] = x[::97]  # x == y cases
+    xs = np.where(np.arange(n) % 3 == 0, -x, x).astype(dt)
+    xs[::1009] = 0
+    ex = ((np.arange(n) * 7919) % 2001 - 1000).astype(np.int64)
+    ey = ((np.arange(n) * 104729) % 2001 - 1000).astype(np.int64)
+    suf = "f64" if dt == np.float64 else "f32"
+    for op in range(7):
+        xf = x if op in (capi.EPAIR_OPLUS, capi.EPAIR_OMINUS) else xs
+        ge, gf, gs = K.epair_op(op, dev(xf), dev(y), dev(ex), dev(ey))
+        we, wf, ws = np.empty(n, np.int64), np.empty_like(x), np.empty(n, np.uint8)
+        getattr(ref, f"epair_{suf}")(op, ex.ctypes.data, xf.ctypes.data, ey.ctypes.data, y.ctypes.data,
+                                     we.ctypes.data, wf.ctypes.data, ws.ctypes.data, n)
+        assert (host(gs) == ws).all(), f"op {op} status"
+        ok = ws == 0
+        assert (host(ge)[ok] == we[ok]).all(), f"op {op} e"
+        _gen.assert_bits_equal(host(gf)[ok], wf[ok], f"op {op} f")
+
+
+# ------------------------------------------------------- classify / phases
+def ref_classify(ref, g):
+    n = g.shape[1]
+    o = {"t": np.empty(n, np.uint8), "s_type": np.empty(n, np.int32), "s": np.empty(n, np.int64),
+         "e_G": np.empty(n, np.int64), "inexact_underflow": np.empty(n, np.uint8), "status": np.empty(n, np.uint8)}
+    gp = np.empty_like(g)
+    co = capi.kog_classify_out(*[o[k].ctypes.data for k in ("t", "s_type", "s", "e_G", "inexact_underflow", "status")])
+    fn = ref.classify_prescale_f64 if g.dtype == np.float64 else ref.classify_prescale_f32
+    fn(C.byref(refbind.mat(g)), C.byref(co), C.byref(refbind.mat(gp)), n)
+    o["gp"] = gp
+    return o
+
+
+@pytest.mark.parametrize("dt", DTS)
+def test_classify_prescale(cuda, ref, dt):
+    """classify_test.cpp: type table, e_G, s, prescale, inexact underflow."""
+    n = 200_000
+    g = _gen.matrices(dt, 0xC1A50002, n)
+    mask = (_gen.draws(7, n, 0) % np.uint64(16)).astype(np.int64)
+    for k, bit in enumerate((1, 4, 2, 8)):  # rows g11,g12,g21,g22 <- bits 0,2,1,3
+        g[k][(mask & bit) == 0] = 0
+    g[:, 0] = [np.finfo(dt).max, np.finfo(dt).smallest_subnormal, np.finfo(dt).smallest_subnormal,
+               np.finfo(dt).smallest_subnormal]
+    g[:, 1] = [np.inf, 0, 0, 1]
+    got = K.classify_prescale(dev(g))
+    want = ref_classify(ref, g)
+    assert (host(got["status"]) == want["status"]).all()
+    ok = want["status"] == 0
+    for k in ("t", "s_type", "s", "e_G", "inexact_underflow"):
+        assert (host(got[k])[ok] == want[k][ok]).all(), k
+    _gen.assert_bits_equal(host(got["gp"])[:, ok].ravel(), want["gp"][:, ok].ravel(), "gp")
+
+
+@pytest.mark.parametrize("dt", DTS)
+@pytest.mark.parametrize("wide", [0, 1])
+def test_urv15(cuda, ref, dt, wide):
+    """urv15 on full matrices (svd2_test.cpp:156-191, 395-428), both wide channels."""
+    n = 200_000
+    p, emax, emin = _gen.FMT[dt]
+    g = np.ascontiguousarray(np.stack([_gen.stratified(dt, 0x57D20006, n, emin, emax - 2, k) for k in range(4)]))
+    g[:, 0] = [2, 1, 1, 2]
+    g[:, 1] = [1, 1, 1, -1]
+    g[:, 2] = [2, 4, 1, 2]
+    opt = K.Options(wide_channel=wide)
+    got = K.urv15(dev(g), opt)
+    rt = capi.kog_urv15_f64 if dt == np.float64 else capi.kog_urv15_f32
+    want = refbind.records(rt, n)
+    (ref.urv15_f64 if dt == np.float64 else ref.urv15_f32)(C.byref(refbind.mat(g)), C.addressof(want), n,
+                                                           C.byref(opt.c()))
+    records_equal(got, want, "urv15")
+
+
+@pytest.mark.parametrize("dt", DTS)
+@pytest.mark.parametrize("opt", ALL_OPTIONS[:4], ids=lambda o: f"cr{o.hypot_is_cr}om{o.ominus_for_d}")
+def test_tri_svd(cuda, ref, dt, opt):
+    """tri_svd / tan2phi (svd2_test.cpp:193-285), every Alg. 1 branch."""
+    n = 200_000
+    p, emax, emin = _gen.FMT[dt]
+    a = _gen.positive(dt, 0x57D20007, n, emin, emax - 2, 0)
+    b = _gen.positive(dt, 0x57D20007, n, emin, emax - 2, 1)
+    c = _gen.positive(dt, 0x57D20007, n, emin, emax - 2, 2)
+    a, c = np.maximum(a, c), np.minimum(a, c)
+    fi = np.finfo(dt)
+    mu, nu = dt(fi.tiny), dt(fi.max)
+    special = [(1, 1, 1), (2, 1, 1), (4, 3, 2), (mu, 1, mu * dt(0.5)), (2 * mu, nu / 2, mu), (2, fi.smallest_subnormal, 1)]
+    for i, (x, y, z) in enumerate(special):
+        a[i], b[i], c[i] = x, y, z
+    a, b, c = a.astype(dt), b.astype(dt), c.astype(dt)
+    t13 = (np.arange(n) % 2).astype(np.uint8)
+    got = K.tri_svd(dev(a), dev(b), dev(c), dev(t13), K_opt(opt))
+    rt = capi.kog_trisvd_f64 if dt == np.float64 else capi.kog_trisvd_f32
+    want = refbind.records(rt, n)
+    (ref.tri_svd_f64 if dt == np.float64 else ref.tri_svd_f32)(a.ctypes.data, b.ctypes.data, c.ctypes.data,
+                                                               t13.ctypes.data, C.addressof(want), n, C.byref(opt))
+    records_equal(got, want, "tri_svd")
+
+
+@pytest.mark.parametrize("dt", DTS)
+def test_compose_left_and_triangularize13(cuda, ref, dt):
+    """compose_left (svd2_test.cpp:287-327) and triangularize13 (123-154)."""
+    n = 200_000
+    tp = (_gen.unit(_gen.draws(1, n, 0)) * 2).astype(dt)
+    tt = _gen.unit(_gen.draws(1, n, 1)).astype(dt)
+    tp[:4] = [np.inf, np.inf, 0, 1]
+    tt[:4] = [1, 1, 0.75, 1]
+    m = (np.arange(n) % 2).astype(np.uint8)
+    gc, gs = K.compose_left(dev(tp), dev(tt), dev(m))
+    wc, ws = np.empty_like(tp), np.empty_like(tp)
+    (ref.compose_left_f64 if dt == np.float64 else ref.compose_left_f32)(tp.ctypes.data, tt.ctypes.data,
+                                                                         m.ctypes.data, wc.ctypes.data,
+                                                                         ws.ctypes.data, n)
+    _gen.assert_bits_equal(host(gc), wc, "compose c")
+    _gen.assert_bits_equal(host(gs), ws, "compose s")
+    types = np.array([7, 11, 13, 14], dtype=np.uint8)[(_gen.draws(2, n, 0) % np.uint64(4)).astype(np.int64)]
+    g = np.ascontiguousarray(np.stack([_gen.stratified(dt, 0x57D20002, n, -40, 40, k) for k in range(4)]))
+    for k, bit in enumerate((1, 4, 2, 8)):
+        g[k][(types & bit) == 0] = 0
+    r, up, vp = K.triangularize13(dev(g), dev(types))
+    wr = np.empty_like(g)
+    wup, wvp = np.empty((n, 4), np.int8), np.empty((n, 4), np.int8)
+    (ref.triangularize13_f64 if dt == np.float64 else ref.triangularize13_f32)(
+        C.byref(refbind.mat(g)), types.ctypes.data, C.byref(refbind.mat(wr)), wup.ctypes.data, wvp.ctypes.data, n)
+    _gen.assert_bits_equal(host(r).ravel(), wr.ravel(), "tri13 R")
+    assert (host(up) == wup).all() and (host(vp) == wvp).all()
+
+
+# --------------------------------------------------------------- svd2
+@pytest.mark.parametrize("dt", DTS)
+@pytest.mark.parametrize("opt", ALL_OPTIONS, ids=lambda o: f"cr{o.hypot_is_cr}om{o.ominus_for_d}w{o.wide_channel}")
+def test_svd2_any_finite_all_options(cuda, ref, dt, opt):
+    """svd2 on any-finite matrices with every Options combination
+    (svd2_test.cpp:329-359, acceptance.cpp:518-561 totality fuzz)."""
+    n = 1 << 18
+    g = _gen.matrices(dt, 0x57D20004, n)
+    mask = (_gen.draws(11, n, 0) % np.uint64(16)).astype(np.int64)
+    sel = (_gen.draws(11, n, 1) % np.uint64(4)) == 0
+    for k, bit in enumerate((1, 4, 2, 8)):
+        g[k][sel & ((mask & bit) == 0)] = 0
+    got = K.svd2(dev(g), K_opt(opt))
+    want = refbind.svd2(ref, g, opt)
+    compare_svd(got, want, "svd2")
+
+
+TARGETED = [  # harness_test.cpp:181-193 + svd2_test.cpp known answers
+    (1, 1, 0, 1), (2, 1, 0, 1), (4, 3, 0, 2), (1, 3, 0, 4), (2, 0, 0, 1), (3, 0, 4, 0), (1, 1, 0, 0),
+    (1, 1, 1, -1), (2, 4, 1, 2), (0, 3, 2, 0), (-5, 0, 0, 0), (2, 1, 1, 2), (0, 2, 0, 1), (0, 0, 0, 0),
+]
+
+
+@pytest.mark.parametrize("dt", DTS)
+def test_svd2_targeted(cuda, ref, dt):
+    fi = np.finfo(dt)
+    mu, nu, mc = fi.tiny, fi.max, fi.smallest_subnormal
+    rows = list(TARGETED) + [(mu, 1, 0, mu / 2), (mu, nu / 4, 0, mu), (mu, 1, 0, 1), (mc, -mc, 3 * mc, 2 * mc),
+                             (nu, mc, mc, mc), (nu, 1, 1, 1)]
+    g = np.ascontiguousarray(np.array(rows, dtype=dt).T)
+    for o in ALL_OPTIONS:
+        compare_svd(K.svd2(dev(g), K_opt(o)), refbind.svd2(ref, g, o), "targeted")
+    r = K.svd2(dev(g))
+    path = (host(r["flags"]).view(np.uint32) >> capi.F_PATH_SHIFT) & 7
+    assert set(path.tolist()) >= {0, 1, 2, 3, 4, 5, 6}
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_svd2_baseline_configs(cuda, ref, k):
+    """BASELINE configs 1-4: on-device generator == host generator and svd2
+    bit-exact on 2^20 matrices of each distribution."""
+    cfg = configs.cfg(k, count=1 << 20)
+    g_dev = K.generate(cfg, 0, cfg.count)
+    g_ref = refbind.generate(ref, cfg.c(), 0, cfg.count)
+    _gen.assert_bits_equal(host(g_dev).ravel(), g_ref.ravel(), f"cfg{k} generate")
+    compare_svd(K.svd2(g_dev), refbind.svd2(ref, g_ref), f"cfg{k} svd2")
+    # a later index window (cfg5 sharding: index offsets must reproduce)
+    off = 123_456_789
+    g2 = K.generate(cfg, off, 4096)
+    _gen.assert_bits_equal(host(g2).ravel(), refbind.generate(ref, cfg.c(), off, 4096).ravel(), "offset window")
+
+
+@pytest.mark.parametrize("dt", DTS)
+def test_svd2_host_pipeline(cuda, ref, dt):
+    """kog_svd2_host_*: host buffers through the chunked H2D/kernel/D2H pipeline."""
+    n = (1 << 22) * 2 + 12345  # several chunks and a ragged tail
+    g = _gen.matrices(dt, 0x51D, n)
+    gt = torch.from_numpy(g).pin_memory()
+    got = K.svd2_host(gt)
+    want = refbind.svd2(ref, g)
+    compare_svd({k: v.numpy() for k, v in got.items()}, want, "svd2_host")
+
+
+def test_empty_and_null(cuda):
+    g = torch.empty((4, 0), dtype=torch.float64, device="cuda")
+    r = K.svd2(g)
+    assert r["flags"].numel() == 0
+    with pytest.raises(capi.KogError):
+        capi.check(capi.load().kog_svd2_batch_f64(None, None, 1, None, None))
+
+
+# ------------------------------------------------------ oracle + metrics
+@pytest.mark.parametrize("dt", DTS)
+def test_svd2_ext_and_metrics(cuda, ref, dt):
+    """svd2_ext and the error measures, bit-exact (oracle_test.cpp surfaces)."""
+    n = 1 << 16
+    g = _gen.matrices(dt, 0xE1F00003, n)
+    mask = (_gen.draws(5, n, 0) % np.uint64(16)).astype(np.int64)
+    for k, bit in enumerate((1, 4, 2, 8)):
+        g[k][(mask & bit) == 0] = 0
+    got = K.svd2_ext(dev(g))
+    want = refbind.records(capi.kog_extsvd, n)
+    (ref.svd2_ext_f64 if dt == np.float64 else ref.svd2_ext_f32)(C.byref(refbind.mat(g)), C.addressof(want), n)
+    records_equal(got, want, "svd2_ext")
+    gm = K.metrics(dev(g))
+    wm = refbind.records(capi.kog_metrics, n)
+    (ref.metrics_f64 if dt == np.float64 else ref.metrics_f32)(C.byref(refbind.mat(g)), C.addressof(wm), n,
+                                                               C.byref(capi.default_options()), 0)
+    gb = np.frombuffer(bytes(gm), dtype=np.uint8).reshape(n, -1)
+    wb = np.frombuffer(bytes(wm), dtype=np.uint8).reshape(n, -1)
+    bad = np.nonzero((gb != wb).any(axis=1))[0]
+    assert bad.size == 0, f"{bad.size} metric records differ; first {bad[0]}: {g[:, bad[0]]}"
+
+
+# ----------------------------------------------------------- harness
+APPENDIX_B = [  # reference CSV rows captured in the survey container
+    "double,gen,circ,0,1048576,0000000000c0ffee,kog,5.262556799095865e-16,4.469753940626907e-16,5.475477442600766e-16,4.740088882553483e-16,4.726642799363624e-16,14512464.951216837",
+    "double,tri,bullet,0,1048576,00000000000005b1,kog,3.6629159219119507e-16,3.1751026529124164e-16,3.3703653551936313e-16,4.657287832316551e-16,4.700986429951113e-16,2.9702909105091426e+1218",
+    "double,gen,bullet,0,1048576,00000000feedbeef,kog,3.366846414194082e-16,3.805030544364915e-16,1,4.689522663061862e-16,4.658513990744075e-16,1.5833298576379424e+615",
+    "double,gen,sigma,1024,1048576,000000000f1e2d3c,kog,3.5758175247668104e-16,3.579491957323541e-16,4.550667095394166e-16,4.646732779855881e-16,4.61552054390659e-16,3.8630772656508938e+306",
+    "single,gen,circ,0,1048576,0000000000c0ffee,kog,2.8583080828580647e-07,2.3807519202657365e-07,3.222986020883533e-07,2.534061500807315e-07,2.5379602539148014e-07,12409701.427193983",
+]
+
+
+def _cfg_of_row(row: str) -> K.RunConfig:
+    f = row.split(",")
+    return K.RunConfig(single_precision=f[0] == "single", shape=capi.SHAPE_TRI if f[1] == "tri" else capi.SHAPE_GEN,
+                       regime={"circ": 0, "bullet": 1, "sigma": 2}[f[2]], varsigma=int(f[3]), count=int(f[4]),
+                       seed=int(f[5], 16), routine=capi.ROUTINE_KOG)
+
+
+@pytest.mark.parametrize("row", APPENDIX_B, ids=lambda r: ",".join(r.split(",")[:3]))
+def test_run_batch_csv_matches_reference_rows(cuda, row):
+    """GPU-backed run_batch + csv_row byte-identical to the reference's rows."""
+    cfg = _cfg_of_row(row)
+    st = K.run_batch(cfg)
+    assert K.csv_row(cfg, st) == row
+
+
+def test_run_batch_vs_reference_counts(cuda, ref):
+    """ErrorStats incl. all 19 BranchCounts equal the reference's run_batch
+    (harness.hpp:226-271) on the branch-coverage batch of harness_test.cpp:164-217."""
+    for cfg in (K.RunConfig(shape=capi.SHAPE_GEN, regime=capi.REGIME_BULLET, count=1 << 18, seed=77),
+                K.RunConfig(shape=capi.SHAPE_TRI, regime=capi.REGIME_CIRC, count=1 << 18, seed=78),
+                K.RunConfig(shape=capi.SHAPE_TRI, regime=capi.REGIME_BULLET, count=50000, seed=0x1234ABCD,
+                            routine=capi.ROUTINE_LASV2),
+                configs.cfg(3, count=1 << 18), configs.cfg(4, count=1 << 18), configs.cfg(2, count=1 << 18)):
+        st = K.run_batch(cfg)
+        rc, want, msg = refbind.run_batch(ref, cfg.c())
+        assert rc == 0, msg
+        got_row, want_row = K.csv_row(cfg, st).split(","), refbind.csv_row(ref, cfg.c(), want).split(",")
+        if cfg.regime == capi.REGIME_RANGED:  # the reference's csv_row has no name for the extension
+            got_row[2] = want_row[2]
+        assert got_row == want_row
+        for f in ("t2p", "path"):
+            assert list(getattr(st, f)) == list(getattr(want, f)), f
+        for f in ("tanpsi_inf", "diag_swap", "compose_minus", "sigma_swap", "prescale_inexact", "kappa_inf"):
+            assert getattr(st, f) == getattr(want, f), f
+        assert (st.max_kappa2.e, st.max_kappa2.hi, st.max_kappa2.lo) == \
+               (want.max_kappa2.e, want.max_kappa2.hi, want.max_kappa2.lo)
+
+
+def test_run_batch_validation_and_empty(cuda):
+    """harness_test.cpp:63-86."""
+    st = K.run_batch(K.RunConfig(shape=capi.SHAPE_TRI, regime=capi.REGIME_BULLET, count=0, seed=1))
+    assert (st.reG, st.reS1, st.reS2, st.reU, st.reV) == (0, 0, 0, 0, 0) and st.max_kappa2.hi == 0
+    with pytest.raises(ValueError):
+        K.run_batch(K.RunConfig(shape=capi.SHAPE_GEN, routine=capi.ROUTINE_LASV2, count=10))
+    with pytest.raises(ValueError):
+        K.run_batch(K.RunConfig(regime=capi.REGIME_SIGMA, varsigma=0, count=10))
+    with pytest.raises(ValueError):
+        K.run_batch(K.RunConfig(regime=capi.REGIME_SIGMA, varsigma=5000, count=10))
+
+
+def test_study_sharding_bit_identical(cuda):
+    """cfg5 sharding: any split of the index range merges to the same stats."""
+    cfg = configs.cfg(5, count=3 * (1 << 16) + 77)
+    whole = K.StudyStats()
+    whole.add(cfg, 0, cfg.count)
+    a = whole.read()
+    cuts = [0, 1000, 70000, 150000, cfg.count]
+    merged = K.new_stats()
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        s = K.StudyStats()
+        s.add(cfg, lo, hi - lo)
+        K.merge_stats(merged, s.read())
+    assert bytes(merged) == bytes(a)
+
+
+@pytest.mark.parametrize("dt", DTS)
+def test_lasv2(cuda, ref, dt):
+    """lasv2_ref on triangular triples (lasv2_test.cpp surfaces)."""
+    n = 200_000
+    p, emax, emin = _gen.FMT[dt]
+    f = _gen.stratified(dt, 0x1A5, n, emin, emax - 2, 0)
+    g = _gen.stratified(dt, 0x1A5, n, emin, emax - 2, 1)
+    h = _gen.stratified(dt, 0x1A5, n, emin, emax - 2, 2)
+    g[::7] = 0
+    got = host(K.lasv2(dev(f), dev(g), dev(h)))
+    want = np.empty((n, 6), dtype=dt)
+    (ref.lasv2_f64 if dt == np.float64 else ref.lasv2_f32)(f.ctypes.data, g.ctypes.data, h.ctypes.data,
+                                                           want.ctypes.data, n)
+    _gen.assert_bits_equal(got.ravel(), want.ravel(), "lasv2")
