@@ -672,7 +672,11 @@ int kogref_run_batch(const kog_run_config* c, kog_stats* out) {
 
 int kogref_csv_row(const kog_run_config* c, const kog_stats* st, char* buf, size_t cap) {
   RunConfig rc = to_rc(c);
-  const std::string row = csv_row(rc, stats_from_c(st));
+  std::string row = csv_row(rc, stats_from_c(st));
+  if (c->regime == KOG_REGIME_RANGED) {  // the extension has no reference name
+    const size_t a = row.find(',', row.find(',') + 1) + 1, b = row.find(',', a);
+    row.replace(a, b - a, "ranged");
+  }
   if (row.size() + 1 > cap) return -1;
   std::memcpy(buf, row.c_str(), row.size() + 1);
   return int(row.size());
