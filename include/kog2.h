@@ -365,6 +365,10 @@ int kog_lasv2_batch_f32(const float* f, const float* g, const float* h, float* o
 /* FP64 pipe probe: a DFMA chain, `iters` per thread over the whole device;
  * writes one value per thread to sink[] so the work cannot be elided. */
 int kog_fp64_probe(double* sink, uint64_t threads, uint32_t iters, void* stream);
+/* Correctly rounded x / y as used on the svd2 path (significand division with
+ * the general IEEE division out of line), exposed for verification. */
+int kog_div_batch_f64(const double* x, const double* y, double* out, uint64_t n, void* stream);
+int kog_div_batch_f32(const float* x, const float* y, float* out, uint64_t n, void* stream);
 /* number of kernel launches issued by this library since load */
 uint64_t kog_launch_count(void);
 

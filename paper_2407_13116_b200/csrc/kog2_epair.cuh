@@ -12,7 +12,7 @@ namespace kog2 {
 // EPair<T> (epair.hpp:16-46)
 template <class T>
 struct EPair {
-  long long e;
+  int e;  // |e| < 2^30 on every path (sigma exponents lie in [-3171, 1024])
   T f;  // 0, or |f| in [1,2)
 };
 
@@ -23,7 +23,7 @@ __device__ __forceinline__ EPair<T> ep_zero() {
 
 // EPair(ee, ff): normalising constructor (epair.hpp:23-36)
 template <class T>
-__device__ __forceinline__ EPair<T> ep_make(long long ee, T ff, unsigned& err) {
+__device__ __forceinline__ EPair<T> ep_make(int ee, T ff, unsigned& err) {
   if (!is_finite(ff)) err |= 1u;
   if (ff == T(0)) return EPair<T>{0, T(0)};
   return EPair<T>{ee + ilogb_nz(ff), mant_nz(ff)};
@@ -58,8 +58,8 @@ __device__ __forceinline__ EPair<T> ominus(T x, T y, unsigned& err) {
   if (x == y) return ep_zero<T>();
   const T z = x - y;
   if (fabs(z) >= FP<T>::norm_min()) return ep_make<T>(0, z, err);
-  const long long ex = split(x).e, ey = split(y).e;
-  const long long c = FP<T>::emin + FP<T>::p - 1 - (ex < ey ? ex : ey);
+  const int ex = static_cast<int>(split(x).e), ey = static_cast<int>(split(y).e);
+  const int c = FP<T>::emin + FP<T>::p - 1 - (ex < ey ? ex : ey);
   const T zs = assemble(c, x) - assemble(c, y);
   return ep_make<T>(-c, zs, err);
 }
@@ -74,7 +74,7 @@ __device__ __forceinline__ EPair<T> ep_mul(const EPair<T>& x, const EPair<T>& y,
 template <class T>
 __device__ __forceinline__ EPair<T> ep_div(const EPair<T>& x, const EPair<T>& y, unsigned& err) {
   if (y.f == T(0)) err |= 1u;
-  return ep_make<T>(x.e - y.e, x.f / y.f, err);
+  return ep_make<T>(x.e - y.e, div_rn(x.f, y.f), err);
 }
 
 // abs / neg (epair.hpp:90-102)
@@ -89,7 +89,7 @@ __device__ __forceinline__ EPair<T> ep_neg(const EPair<T>& x) {
 
 // scale2 (epair.hpp:104-110): exact multiplication by 2^k
 template <class T>
-__device__ __forceinline__ EPair<T> scale2(long long k, const EPair<T>& x) {
+__device__ __forceinline__ EPair<T> scale2(int k, const EPair<T>& x) {
   EPair<T> r = x;
   if (r.f != T(0)) r.e += k;
   return r;

@@ -15,6 +15,10 @@ __global__ void k_hypot(const T* a, const T* b, T* o, uint64_t n) {
   for (uint64_t i = gtid(); i < n; i += gstride()) o[i] = hypot_cr(a[i], b[i]);
 }
 template <class T>
+__global__ void k_div(const T* a, const T* b, T* o, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) o[i] = div_rn(a[i], b[i]);
+}
+template <class T>
 __global__ void k_split(const T* x, int64_t* e, T* f, uint64_t n) {
   for (uint64_t i = gtid(); i < n; i += gstride()) {
     const Split<T> s = split(x[i]);
@@ -42,6 +46,12 @@ __global__ void k_epair(int op, const int64_t* xe, const T* xf, const int64_t* y
     unsigned err = 0;
     const long long xee = xe ? xe[i] : 0, yee = ye ? ye[i] : 0;
     const T xff = xf[i], yff = yf ? yf[i] : T(0);
+    if (xee > (1 << 30) || xee < -(1 << 30) || yee > (1 << 30) || yee < -(1 << 30)) {
+      st[i] = 2;  // exponent outside the supported |e| <= 2^30 (include/kog2.h)
+      oe[i] = 0;
+      of[i] = T(0);
+      continue;
+    }
     EPair<T> r = ep_zero<T>();
     bool value_out = false;
     T val = T(0);
@@ -377,6 +387,15 @@ int kog_generate_batch_f64(const kog_run_config* cfg, uint64_t index0, const kog
 int kog_generate_batch_f32(const kog_run_config* cfg, uint64_t index0, const kog_mat_f32* out, uint64_t n,
                            void* stream) {
   return launch_generate<float>(cfg, index0, out, n, KOG2_ST(stream));
+}
+
+int kog_div_batch_f64(const double* x, const double* y, double* out, uint64_t n, void* stream) {
+  if (!x || !y || !out) return kog2_arg_error("kog_div_batch: null argument");
+  KOG_LAUNCH("k_div", k_div<double>, x, y, out)
+}
+int kog_div_batch_f32(const float* x, const float* y, float* out, uint64_t n, void* stream) {
+  if (!x || !y || !out) return kog2_arg_error("kog_div_batch: null argument");
+  KOG_LAUNCH("k_div", k_div<float>, x, y, out)
 }
 
 int kog_fp64_probe(double* sink, uint64_t threads, uint32_t iters, void* stream) {

@@ -26,7 +26,7 @@ __device__ __forceinline__ bool all_finite(const Mat<T>& g) {  // classify.hpp:2
 struct TypeInfo {  // classify.hpp:29-35
   unsigned t;
   int s_type;
-  long long s;
+  int s;
   long long e_G;
 };
 
@@ -52,7 +52,7 @@ __device__ __forceinline__ TypeInfo classify(const Mat<T>& g, unsigned& err) {
   if (g.g12 != T(0)) eg = max(eg, ilogb_nz(g.g12));
   if (g.g22 != T(0)) eg = max(eg, ilogb_nz(g.g22));
   info.e_G = info.t == 0 ? KOG2_EXP_SENTINEL : static_cast<long long>(eg);
-  info.s = info.t == 0 ? 0 : static_cast<long long>(FP<T>::emax - eg - info.s_type);
+  info.s = info.t == 0 ? 0 : FP<T>::emax - eg - info.s_type;
   return info;
 }
 
@@ -65,7 +65,7 @@ __device__ __forceinline__ unsigned type_of(const Mat<T>& g) {
 
 // prescale (classify.hpp:60-78)
 template <class T>
-__device__ __forceinline__ Mat<T> prescale(const Mat<T>& g, long long s, bool& inexact) {
+__device__ __forceinline__ Mat<T> prescale(const Mat<T>& g, int s, bool& inexact) {
   Mat<T> gp{assemble(s, g.g11), assemble(s, g.g12), assemble(s, g.g21), assemble(s, g.g22)};
   inexact = false;
   if (s < 0)
@@ -157,7 +157,7 @@ template <class T>
 struct Result {  // Svd2Result<T> (svd2.hpp:134-140)
   Mat<T> u, v;
   EPair<T> sigma1, sigma2;
-  long long s;
+  int s;
   unsigned flags;  // trace bits + KOG_F_DOMAIN_ERROR; sign bits added at store
 };
 
@@ -167,7 +167,7 @@ __device__ __forceinline__ unsigned tr_t2p(unsigned b) { return b << KOG_F_T2P_S
 // ------------------------------------------------------------ phase 1
 // svd_simple (svd2.hpp:145-182): t' ~ 9, exact SVD by permutations and signs
 template <class T>
-__device__ __forceinline__ void svd_simple(const Mat<T>& a, long long s, unsigned t, unsigned flags,
+__device__ __forceinline__ void svd_simple(const Mat<T>& a, int s, unsigned t, unsigned flags,
                                            Result<T>& out) {
   flags |= tr_path(KOG_PATH_SIMPLE);
   SP pu = sp_identity(), pv = sp_identity();
@@ -193,13 +193,13 @@ __device__ __forceinline__ void svd_simple(const Mat<T>& a, long long s, unsigne
 // Rot / rot_from_tan_sec (svd2.hpp:186-195)
 template <class T>
 __device__ __forceinline__ Mat<T> rot_mat(T tan, T sec) {
-  const T c = T(1) / sec, s = tan / sec;
+  const T c = div_rn(T(1), sec), s = div_rn(tan, sec);
   return Mat<T>{c, -s, s, c};
 }
 
 // svd_mono (svd2.hpp:199-244): t' ~ 3 or 5, one Givens rotation
 template <class T>
-__device__ __forceinline__ void svd_mono(const Mat<T>& gp, long long s, unsigned t, unsigned flags,
+__device__ __forceinline__ void svd_mono(const Mat<T>& gp, int s, unsigned t, unsigned flags,
                                          Result<T>& out) {
   unsigned err = 0;
   out.s = s;
@@ -212,7 +212,7 @@ __device__ __forceinline__ void svd_mono(const Mat<T>& gp, long long s, unsigned
     const bool swap = a.g11 < a.g21;
     const SP pu = swap ? sp_exchange() : sp_identity();
     a = apply_left(pu, a);
-    const T tan = a.g21 / a.g11;
+    const T tan = div_rn(a.g21, a.g11);
     const T sec = sec_from_tan(tan);
     const T sig1 = hypot_cr(a.g11, a.g21);
     const Mat<T> uth = rot_mat(tan, sec);
@@ -228,7 +228,7 @@ __device__ __forceinline__ void svd_mono(const Mat<T>& gp, long long s, unsigned
     const bool swap = a.g11 < a.g12;
     const SP pvo = swap ? sp_exchange() : sp_identity();
     a = apply_right(a, pvo);
-    const T tan = a.g12 / a.g11;
+    const T tan = div_rn(a.g12, a.g11);
     const T sec = sec_from_tan(tan);
     const T sig1 = hypot_cr(a.g11, a.g12);
     const Mat<T> vth = rot_mat(tan, sec);
@@ -284,12 +284,12 @@ __device__ __forceinline__ T wide_dot2_div(T a, T b, T c, T d, T q1, T q2, int W
     const T w = c1 * d1;
     const T e = fma(c1, d1, -w);
     const T f = fma(a1, b1, w);
-    return scalbn_t((f + e) / qs, scale - kq) / q2;
+    return div_rn(scalbn_t(div_rn(f + e, qs), scale - kq), q2);
   }
   if (FP<T>::p == 24) {
     const double num = static_cast<double>(a1) * static_cast<double>(b1) +
                        static_cast<double>(c1) * static_cast<double>(d1);
-    return scalbn_t(static_cast<T>(num / static_cast<double>(qs)), scale - kq) / q2;
+    return div_rn(scalbn_t(static_cast<T>(div_rn(num, static_cast<double>(qs))), scale - kq), q2);
   } else {
     double p1, e1, p2, e2;
     two_prod(static_cast<double>(a1), static_cast<double>(b1), p1, e1);
@@ -302,9 +302,9 @@ __device__ __forceinline__ T wide_dot2_div(T a, T b, T c, T d, T q1, T q2, int W
     s2 += t2;
     fast_two_sum(s1, s2, s1, s2);
     const double qd = static_cast<double>(qs);
-    const double h = s1 / qd;
+    const double h = div_rn(s1, qd);
     const double rem = fma(-h, qd, s1) + s2;
-    return static_cast<T>(scalbn_d(h + rem / qd, scale - kq)) / q2;
+    return div_rn(static_cast<T>(scalbn_d(h + div_rn(rem, qd), scale - kq)), q2);
   }
 }
 
@@ -338,16 +338,16 @@ __device__ __forceinline__ Urv15<T> urv15(const Mat<T>& gp, const Opt& o) {
   if (out.row_swap) a = Mat<T>{a.g21, a.g22, a.g11, a.g12};
   out.gppp = a;
 
-  out.tan_theta = a.g21 / a.g11;
+  out.tan_theta = div_rn(a.g21, a.g11);
   out.sec_theta = sec_from_tan(out.tan_theta);
   out.r11 = w1p;
   const bool same_sign = sign_bit(a.g12) == sign_bit(a.g22);
   if (same_sign) {
-    out.r12_raw = fma(a.g22, out.tan_theta, a.g12) / out.sec_theta;
+    out.r12_raw = div_rn(fma(a.g22, out.tan_theta, a.g12), out.sec_theta);
     out.r22_raw = wide_dot2_div<T>(a.g22, a.g11, -a.g12, a.g21, a.g11, out.sec_theta, o.wc);
     out.ext_is_r22 = true;
   } else {
-    out.r22_raw = fma(-a.g12, out.tan_theta, a.g22) / out.sec_theta;
+    out.r22_raw = div_rn(fma(-a.g12, out.tan_theta, a.g22), out.sec_theta);
     out.r12_raw = wide_dot2_div<T>(a.g12, a.g11, a.g22, a.g21, a.g11, out.sec_theta, o.wc);
     out.ext_is_r22 = false;
   }
@@ -383,25 +383,25 @@ __device__ __forceinline__ T tan2phi(T r11, T r12, T r22, bool t13, const Opt& o
                                      unsigned& err) {
   if (r11 == r22) {
     branch = KOG_T2P_DIAG_EQUAL;
-    return (T(2) * r22) / r12;
+    return div_rn(T(2) * r22, r12);
   }
   if (r12 == r22) {
     branch = KOG_T2P_OFFDIAG_EQUAL;
     const EPair<T> num = scale2(1, ep_mul(ep_make<T>(0, r12, err), ep_make<T>(0, r22, err), err));
     return ep_value(ep_div(num, ep_mul(ep_make<T>(0, r11, err), ep_make<T>(0, r11, err), err), err));
   }
-  if (t13 && r11 / r12 < FP<T>::unit_roundoff()) {
+  if (t13 && div_rn(r11, r12) < FP<T>::unit_roundoff()) {
     branch = KOG_T2P_SMALL_RATIO;
-    return (T(2) * r22) / r12;
+    return div_rn(T(2) * r22, r12);
   }
   if (!o.hcr) {
     branch = KOG_T2P_FALLBACK;
     if (r11 > r12) {
-      const T x = r12 / r11, y = r22 / r11;
-      return ((T(2) * x) * y) / std_max(fma(x - y, x + y, T(1)), T(0));
+      const T x = div_rn(r12, r11), y = div_rn(r22, r11);
+      return div_rn((T(2) * x) * y, std_max(fma(x - y, x + y, T(1)), T(0)));
     }
-    const T x = r11 / r12, y = r22 / r12;
-    return (T(2) * y) / std_max(fma(x - y, x + y, T(1)), T(0));
+    const T x = div_rn(r11, r12), y = div_rn(r22, r12);
+    return div_rn(T(2) * y, std_max(fma(x - y, x + y, T(1)), T(0)));
   }
   const T h = hypot_cr(r11, r12);
   if (h == r22) {
@@ -435,12 +435,12 @@ __device__ __forceinline__ TriSvd<T> tri_svd(T r11, T r12, T r22, bool t13, cons
   out.t2f = t2f;
   out.tan_phi = tan_from_double_angle(t2f);
   out.sec_phi = sec_from_tan(out.tan_phi);
-  out.cos_phi = T(1) / out.sec_phi;
-  out.sin_phi = out.tan_phi / out.sec_phi;
+  out.cos_phi = div_rn(T(1), out.sec_phi);
+  out.sin_phi = div_rn(out.tan_phi, out.sec_phi);
 
   const EPair<T> r11p = ep_make<T>(0, r11, err), r22p = ep_make<T>(0, r22, err);
   const T t = fma(r22, out.tan_phi, r12);
-  out.tan_psi = t / r11;
+  out.tan_psi = div_rn(t, r11);
   if (is_inf(out.tan_psi)) {
     out.tanpsi_inf = true;
     const EPair<T> tp = ep_make<T>(0, t, err);
@@ -453,8 +453,8 @@ __device__ __forceinline__ TriSvd<T> tri_svd(T r11, T r12, T r22, bool t13, cons
   } else {
     out.tanpsi_inf = false;
     out.sec_psi = sec_from_tan(out.tan_psi);
-    out.cos_psi = T(1) / out.sec_psi;
-    out.sin_psi = out.tan_psi / out.sec_psi;
+    out.cos_psi = div_rn(T(1), out.sec_psi);
+    out.sin_psi = div_rn(out.tan_psi, out.sec_psi);
     const EPair<T> ratio = ep_div(ep_make<T>(0, out.sec_phi, err), ep_make<T>(0, out.sec_psi, err), err);
     out.sig1 = ep_div(r11p, ratio, err);
     out.sig2 = ep_mul(r22p, ratio, err);
@@ -476,16 +476,16 @@ __device__ __forceinline__ void compose_left(T tan_phi_bold, T tan_theta, bool m
   T tanchi;
   bool beyond_quarter;
   if (is_inf(tan_phi_bold)) {
-    tanchi = (minus_form ? T(1) : T(-1)) / tan_theta;
+    tanchi = div_rn(minus_form ? T(1) : T(-1), tan_theta);
     beyond_quarter = !minus_form;
   } else {
     const T num = minus_form ? tan_phi_bold - tan_theta : tan_phi_bold + tan_theta;
     const T den = minus_form ? fma(tan_phi_bold, tan_theta, T(1)) : fma(-tan_phi_bold, tan_theta, T(1));
     if (is_inf(den)) {
-      const T q = T(1) / tan_theta;
+      const T q = div_rn(T(1), tan_theta);
       tanchi = sign_bit(den) ? -fabs(q) : fabs(q);  // std::copysign(1/tan_theta, den)
     } else {
-      tanchi = num / den;
+      tanchi = div_rn(num, den);
     }
     beyond_quarter = !minus_form && den < T(0);
   }
@@ -494,8 +494,8 @@ __device__ __forceinline__ void compose_left(T tan_phi_bold, T tan_theta, bool m
     rs = sign_bit(tanchi) ? T(-1) : T(1);
   } else {
     const T sec = sec_from_tan(tanchi);
-    rc = T(1) / sec;
-    rs = tanchi / sec;
+    rc = div_rn(T(1), sec);
+    rs = div_rn(tanchi, sec);
   }
   if (beyond_quarter) {
     rc = -rc;
@@ -517,7 +517,7 @@ struct LeftFactor {
 // assemble_svd (svd2.hpp:547-598)
 template <class T>
 __device__ __forceinline__ void assemble_svd(const Mat<T>& r, const LeftFactor<T>& left,
-                                             const SP& vplus, long long s, bool t13, const Opt& o,
+                                             const SP& vplus, int s, bool t13, const Opt& o,
                                              unsigned flags, Result<T>& out) {
   const bool diag_swap = r.g11 < r.g22;
   if (diag_swap) flags |= KOG_F_DIAG_SWAP;
@@ -539,7 +539,7 @@ __device__ __forceinline__ void assemble_svd(const Mat<T>& r, const LeftFactor<T
                                   : Mat<T>{ts.cos_phi, -ts.sin_phi, ts.sin_phi, ts.cos_phi};
     u = apply_left(left.uplus, urot);
   } else {
-    const T tan_phi_bold = diag_swap ? T(1) / ts.tan_psi : ts.tan_phi;
+    const T tan_phi_bold = diag_swap ? div_rn(T(1), ts.tan_psi) : ts.tan_phi;
     const bool minus_form = left.s22 < 0;
     if (minus_form) flags |= KOG_F_COMPOSE_MINUS;
     T cc, cs;
@@ -590,30 +590,33 @@ __device__ __forceinline__ void svd2(const Mat<T>& g, const Opt& o, Result<T>& o
     svd_mono(gp, info.s, t1, flags, out);
     return;
   }
+  // Both triangular routes (t' ~ 13 and the non-degenerate t' = 15) end in the
+  // same assemble_svd (svd2.hpp:627, 647); it is called from one site here so
+  // a warp mixing the two routes runs the triangular SVD once, converged.
+  Mat<T> r;
+  LeftFactor<T> left;
+  SP vplus;
+  bool t13;
+  Urv15<T> urv;
   if (t1 != 15) {
     flags |= tr_path(KOG_PATH_TRI13);
     const Tri13<T> tri = triangularize13(gp, t1);
-    LeftFactor<T> left;
+    r = tri.r;
     left.composed = false;
     left.uplus = tri.uplus;
     left.sr0 = left.sr1 = 1;
     left.row_swap = false;
     left.tan_theta = T(0);
     left.s22 = 1;
-    assemble_svd<T>(tri.r, left, tri.vplus, info.s, true, o, flags, out);
-    return;
-  }
-
-  const Urv15<T> urv = urv15<T>(gp, o);
-  if (urv.col_swap) flags |= KOG_F_URV_COL_SWAP;
-  if (urv.row_swap) flags |= KOG_F_URV_ROW_SWAP;
-  const SP pu = urv.row_swap ? sp_exchange() : sp_identity();
-  const SP s1 = sp_row_signs(urv.sr0, urv.sr1);
-  const SP pv = urv.col_swap ? sp_exchange() : sp_identity();
-
-  if (urv.next == 0) {
+    vplus = tri.vplus;
+    t13 = true;
+    urv.next = 0;
+  } else {
+    urv = urv15<T>(gp, o);
+    if (urv.col_swap) flags |= KOG_F_URV_COL_SWAP;
+    if (urv.row_swap) flags |= KOG_F_URV_ROW_SWAP;
     flags |= tr_path(KOG_PATH_URV15);
-    LeftFactor<T> left;
+    r = urv.r;
     left.composed = true;
     left.uplus = sp_identity();
     left.sr0 = urv.sr0;
@@ -621,12 +624,19 @@ __device__ __forceinline__ void svd2(const Mat<T>& g, const Opt& o, Result<T>& o
     left.row_swap = urv.row_swap;
     left.tan_theta = urv.tan_theta;
     left.s22 = urv.s22;
-    const SP vplus = sp_mul(pv, sp_row_signs(1, urv.s12));
-    assemble_svd<T>(urv.r, left, vplus, info.s, false, o, flags, out);
+    vplus = sp_mul(urv.col_swap ? sp_exchange() : sp_identity(), sp_row_signs(1, urv.s12));
+    t13 = false;
+  }
+  if (urv.next == 0) {
+    assemble_svd<T>(r, left, vplus, info.s, t13, o, flags, out);
     return;
   }
 
   // degenerate triangle (svd2.hpp:650-686)
+  flags &= ~(7u << KOG_F_PATH_SHIFT);
+  const SP pu = urv.row_swap ? sp_exchange() : sp_identity();
+  const SP s1 = sp_row_signs(urv.sr0, urv.sr1);
+  const SP pv = urv.col_swap ? sp_exchange() : sp_identity();
   const Mat<T> uth = rot_mat(urv.tan_theta, urv.sec_theta);
   const Mat<T> uleft = apply_left(s1, apply_left(pu, uth));
   out.s = info.s;
@@ -656,7 +666,7 @@ __device__ __forceinline__ void svd2(const Mat<T>& g, const Opt& o, Result<T>& o
       b = tmp;
     }
     const SP pvo = ord_swap ? sp_exchange() : sp_identity();
-    const T tan = b / a;
+    const T tan = div_rn(b, a);
     const T sec = sec_from_tan(tan);
     const Mat<T> vth = rot_mat(tan, sec);
     out.u = uleft;

@@ -119,6 +119,39 @@ def test_hypot_adversarial_edges(cuda, ref, dt):
 
 
 @pytest.mark.parametrize("dt", DTS)
+def test_division_correctly_rounded(cuda, dt):
+    """div_rn (the division every svd2 quotient uses) == IEEE x / y (numpy),
+    on any-finite pairs, significand-only pairs and near-1/near-2 patterns."""
+    n = 4_000_000
+    x = _gen.any_finite(dt, 0xD1F, n, 0)
+    y = _gen.any_finite(dt, 0xD1F, n, 1)
+    p = 53 if dt == np.float64 else 24
+    ut = np.uint64 if dt == np.float64 else np.uint32
+    one = np.array([1.0], dtype=dt).view(ut)[0]
+    m = _gen.draws(0xD20, n, 0) >> np.uint64(64 - (p - 1))
+    k = _gen.draws(0xD20, n, 1) >> np.uint64(64 - (p - 1))
+    xm = (one | m.astype(ut)).view(dt)
+    ym = (one | k.astype(ut)).view(dt)
+    lo_bits = (np.arange(n) % 64).astype(ut)
+    near = (one | lo_bits).view(dt)  # 1 + j ulp
+    far = (np.array([np.nextafter(dt(2), dt(0))], dt).view(ut)[0] - lo_bits).view(dt)  # 2 - j ulp
+    cases = [(x, y), (xm, ym), (near, far), (far, near), (xm * dt(2.0) ** 900 if dt == np.float64 else xm * dt(2.0) ** 100, ym)]
+    for a, b in cases:
+        a, b = np.ascontiguousarray(a, dtype=dt), np.ascontiguousarray(b, dtype=dt)
+        got = torch.empty(n, dtype=TDT[dt], device="cuda")
+        da, db = dev(a), dev(b)  # keep both alive across the launch
+        capi.check(getattr(capi.load(), f"kog_div_batch_{'f64' if dt == np.float64 else 'f32'}")(
+            da.data_ptr(), db.data_ptr(), got.data_ptr(), n, torch.cuda.current_stream().cuda_stream))
+        with np.errstate(all="ignore"):
+            want = a / b
+        g = host(got)
+        nan = np.isnan(want)
+        bad = np.nonzero(np.isnan(g) != nan)[0]
+        assert bad.size == 0, f"{bad.size} NaN mismatches, first {a[bad[0]]!r} / {b[bad[0]]!r} -> {g[bad[0]]!r}"
+        _gen.assert_bits_equal(g[~nan], want[~nan], "div_rn")
+
+
+@pytest.mark.parametrize("dt", DTS)
 def test_split_assemble_tan_sec(cuda, ref, dt):
     """fpcore_test.cpp:115-213 surfaces, bit-exact against the reference."""
     n = 300_000
