@@ -22,11 +22,27 @@ __device__ __forceinline__ EPair<T> ep_zero() {
 }
 
 // EPair(ee, ff): normalising constructor (epair.hpp:23-36)
+// zero / subnormal / non-finite mantissas (rare; out of line)
+template <class T>
+static __device__ __noinline__ EPair<T> ep_make_rare(int ee, T ff) {
+  if (ff == T(0) || !is_finite(ff)) return EPair<T>{0, T(0)};
+  return EPair<T>{ee + ilogb_nz(ff), mant_nz(ff)};
+}
+__device__ __forceinline__ EPair<double> ep_make_(int ee, double ff, unsigned& err) {
+  const int h = hiw(ff), e = bexp(h);
+  if (normal_bexp(e)) return EPair<double>{ee + e - 1023, sethi(ff, (h & 0x800fffff) | 0x3ff00000)};
+  if (e == 0x7ff) err |= 1u;  // the reference throws on a NaN/inf mantissa
+  return ep_make_rare<double>(ee, ff);
+}
+__device__ __forceinline__ EPair<float> ep_make_(int ee, float ff, unsigned& err) {
+  const int b = __float_as_int(ff), e = bexpf(b);
+  if (normal_bexpf(e)) return EPair<float>{ee + e - 127, __int_as_float((b & 0x807fffff) | 0x3f800000)};
+  if (e == 0xff) err |= 1u;
+  return ep_make_rare<float>(ee, ff);
+}
 template <class T>
 __device__ __forceinline__ EPair<T> ep_make(int ee, T ff, unsigned& err) {
-  if (!is_finite(ff)) err |= 1u;
-  if (ff == T(0)) return EPair<T>{0, T(0)};
-  return EPair<T>{ee + ilogb_nz(ff), mant_nz(ff)};
+  return ep_make_(ee, ff, err);
 }
 
 // value() (epair.hpp:40)

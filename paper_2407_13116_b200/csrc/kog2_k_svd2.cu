@@ -3,6 +3,8 @@
 // layout of include/kog2.h.  The default Options are a compile-time constant
 // (branches on them fold away); any other Options run the same code with the
 // values read from the kernel argument.
+#include <cstdlib>
+
 #include "kog2_common.cuh"
 
 using namespace kog2;
@@ -28,8 +30,8 @@ __device__ __forceinline__ uint32_t sign_flags(const Result<T>& r) {
   return f;
 }
 
-template <class T, bool DEF>
-__global__ void __launch_bounds__(kThreads) k_svd2(InP<T> in, OutP<T> out, uint64_t n, Opt ropt) {
+template <class T, bool DEF, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_svd2(InP<T> in, OutP<T> out, uint64_t n, Opt ropt) {
   const Opt o = DEF ? opt_default() : ropt;
   for (uint64_t i = gtid(); i < n; i += gstride()) {
     const Mat<T> g{ld_cs(in.g11 + i), ld_cs(in.g12 + i), ld_cs(in.g21 + i), ld_cs(in.g22 + i)};
@@ -59,10 +61,18 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
     return kog2_arg_error("kog_svd2_batch: null array pointer");
   const Opt o = opt_of(opt);
   const int grid = grid_for(n);
-  if (opt_is_default(o))
-    k_svd2<T, true><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
+  static const int minb = [] {  // occupancy variant (tuning knob, default 2)
+    const char* e = std::getenv("KOG2_SVD2_MINB");
+    return e ? std::atoi(e) : 3;
+  }();
+  if (!opt_is_default(o))
+    k_svd2<T, false, 2><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
+  else if (minb >= 4)
+    k_svd2<T, true, 4><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
+  else if (minb == 3)
+    k_svd2<T, true, 3><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
   else
-    k_svd2<T, false><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
+    k_svd2<T, true, 2><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
   return launched("k_svd2");
 }
 

@@ -93,9 +93,11 @@ __device__ __forceinline__ Mat<T> sp_mat(const SP& a) {  // as_matrix: zeros are
 }
 
 // x * T(s) for s = +-1: exact; equal to a conditional sign flip on non-NaN x
-template <class T>
-__device__ __forceinline__ T sgnmul(int s, T x) {
-  return s < 0 ? -x : x;
+__device__ __forceinline__ double sgnmul(int s, double x) {  // s = +-1: flip the sign bit
+  return sethi(x, hiw(x) ^ (s & 0x80000000));
+}
+__device__ __forceinline__ float sgnmul(int s, float x) {
+  return __int_as_float(__float_as_int(x) ^ (s & 0x80000000));
 }
 
 // apply_left (svd2.hpp:50-67): s * g, error-free
