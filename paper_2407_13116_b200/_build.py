@@ -54,32 +54,41 @@ def _run(cmd: list[str], log: str | None = None) -> None:
         raise RuntimeError("build failed: " + " ".join(cmd))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJDIR, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: list[str] | None = None) -> str:
+    """Build lib/libkog2.so, or lib/libkog2_<variant>.so with extra -D defines
+    (tuning experiments; select at run time with KOG2_LIB=<path>)."""
+    objdir = OBJDIR if not variant else OBJDIR + "_" + variant
+    lib = LIB if not variant else os.path.join(LIBDIR, f"libkog2_{variant}.so")
+    dflags = [f"-D{d}" for d in (defines or [])]
+    os.makedirs(objdir, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
     common = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "kog2.h")]
     jobs = []
     objs = []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJDIR, src + ".o")
+        o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _newer(o, [s] + common):
-            jobs.append(([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o], o + ".log"))
+            jobs.append(([NVCC] + NVCC_FLAGS + dflags + ["-c", s, "-o", o], o + ".log"))
     for src in CXX_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJDIR, src + ".o")
+        o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _newer(o, [s] + common):
-            jobs.append((["g++"] + CXX_FLAGS + ["-c", s, "-o", o], o + ".log"))
+            jobs.append((["g++"] + CXX_FLAGS + dflags + ["-c", s, "-o", o], o + ".log"))
     with ThreadPoolExecutor(max_workers=4) as ex:
         list(ex.map(lambda j: _run(*j), jobs))
-    if force or jobs or _newer(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lpthread"])
+    if force or jobs or _newer(lib, objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lpthread"])
     if verbose:
-        print("built", LIB)
-    return LIB
+        print("built", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    build(force="--force" in args, verbose=True, variant=var, defines=defs)

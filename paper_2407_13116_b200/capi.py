@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libkog2.so")
+LIB_PATH = os.environ.get("KOG2_LIB") or os.path.join(HERE, "lib", "libkog2.so")
 
 # ---------------------------------------------------------------- constants
 KOG_OK, KOG_ERR_ARG, KOG_ERR_CUDA, KOG_ERR_NODEV, KOG_ERR_ABORT = 0, -1, -2, -3, -4
