@@ -369,6 +369,10 @@ int kog_fp64_probe(double* sink, uint64_t threads, uint32_t iters, void* stream)
  * the general IEEE division out of line), exposed for verification. */
 int kog_div_batch_f64(const double* x, const double* y, double* out, uint64_t n, void* stream);
 int kog_div_batch_f32(const float* x, const float* y, float* out, uint64_t n, void* stream);
+/* Matrices of the last kog_svd2_batch_f64 launch pair (default Options) on the
+ * current device and calling thread that left the specialised path and were
+ * recomputed by the general kernel (synchronous; -1 if none ran yet). */
+int64_t kog_svd2_deferred_count(void);
 /* number of kernel launches issued by this library since load */
 uint64_t kog_launch_count(void);
 

@@ -25,6 +25,7 @@ __device__ __forceinline__ EPair<T> ep_zero() {
 // zero / subnormal / non-finite mantissas (rare; out of line)
 template <class T>
 static __device__ __noinline__ EPair<T> ep_make_rare(int ee, T ff) {
+  KOG2_RARE(5);
   if (ff == T(0) || !is_finite(ff)) return EPair<T>{0, T(0)};
   return EPair<T>{ee + ilogb_nz(ff), mant_nz(ff)};
 }
@@ -32,7 +33,7 @@ __device__ __forceinline__ EPair<double> ep_make_(int ee, double ff, unsigned& e
   const int h = hiw(ff), e = bexp(h);
   if (normal_bexp(e)) return EPair<double>{ee + e - 1023, sethi(ff, (h & 0x800fffff) | 0x3ff00000)};
   if (e == 0x7ff) err |= 1u;  // the reference throws on a NaN/inf mantissa
-  return ep_make_rare<double>(ee, ff);
+  return ep_make_rare<double>(ee, ff);  // zero (canonical pair) or subnormal
 }
 __device__ __forceinline__ EPair<float> ep_make_(int ee, float ff, unsigned& err) {
   const int b = __float_as_int(ff), e = bexpf(b);

@@ -1,11 +1,20 @@
-// kog2_k_svd2.cu — the hot kernel: batched svd2 (svd2.hpp:603-687) over
+// kog2_k_svd2.cu — the hot kernels: batched svd2 (svd2.hpp:603-687) over
 // structure-of-arrays device buffers, one thread per matrix, compact result
-// layout of include/kog2.h.  The default Options are a compile-time constant
-// (branches on them fold away); any other Options run the same code with the
-// values read from the kernel argument.
+// layout of include/kog2.h.
+//
+// binary64 with the default Options runs in two stream-ordered launches:
+//   k_svd2_fast  the specialised straight-line path (kog2_fast.cuh) over the
+//                whole batch; every lane writes its result, and lanes whose
+//                input leaves that path's domain append their index to a
+//                compacted list (one warp-aggregated atomic per warp);
+//   k_svd2_list  the general algorithm (kog2_svd2.cuh) over the listed
+//                indices only, overwriting those results — full warps of
+//                deferred work instead of divergent lanes in every warp.
+// Other Options and binary32 run the general kernel over the batch.
 #include <cstdlib>
 
 #include "kog2_common.cuh"
+#include "kog2_fast.cuh"
 
 using namespace kog2;
 
@@ -30,25 +39,95 @@ __device__ __forceinline__ uint32_t sign_flags(const Result<T>& r) {
   return f;
 }
 
-template <class T, bool DEF, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_svd2(InP<T> in, OutP<T> out, uint64_t n, Opt ropt) {
+template <class T>
+__device__ __forceinline__ void store_result(const OutP<T>& out, uint64_t i, const Result<T>& r) {
+  st_cs(out.sig1_f + i, r.sigma1.f);
+  st_cs(out.sig2_f + i, r.sigma2.f);
+  st_cs(out.sig1_e + i, static_cast<int32_t>(r.sigma1.e));
+  st_cs(out.sig2_e + i, static_cast<int32_t>(r.sigma2.e));
+  st_cs(out.u11 + i, r.u.g11);
+  st_cs(out.u12 + i, r.u.g12);
+  st_cs(out.v11 + i, r.v.g11);
+  st_cs(out.v12 + i, r.v.g12);
+  st_cs(out.s + i, static_cast<int32_t>(r.s));
+  st_cs(out.flags + i, r.flags | sign_flags(r));
+}
+
+// the general algorithm over the whole batch
+template <class T, bool DEF>
+__global__ void __launch_bounds__(kThreads, 3) k_svd2(InP<T> in, OutP<T> out, uint64_t n, Opt ropt) {
   const Opt o = DEF ? opt_default() : ropt;
   for (uint64_t i = gtid(); i < n; i += gstride()) {
     const Mat<T> g{ld_cs(in.g11 + i), ld_cs(in.g12 + i), ld_cs(in.g21 + i), ld_cs(in.g22 + i)};
     Result<T> r;
     svd2<T>(g, o, r);
-    st_cs(out.sig1_f + i, r.sigma1.f);
-    st_cs(out.sig2_f + i, r.sigma2.f);
-    st_cs(out.sig1_e + i, static_cast<int32_t>(r.sigma1.e));
-    st_cs(out.sig2_e + i, static_cast<int32_t>(r.sigma2.e));
-    st_cs(out.u11 + i, r.u.g11);
-    st_cs(out.u12 + i, r.u.g12);
-    st_cs(out.v11 + i, r.v.g11);
-    st_cs(out.v12 + i, r.v.g12);
-    st_cs(out.s + i, static_cast<int32_t>(r.s));
-    st_cs(out.flags + i, r.flags | sign_flags(r));
+    store_result(out, i, r);
   }
 }
+
+// the specialised path; deferred indices go to list[0 .. *count)
+__global__ void __launch_bounds__(kThreads, 3)
+    k_svd2_fast(InP<double> in, OutP<double> out, uint64_t n, uint32_t* list, unsigned* count) {
+  const unsigned lane = threadIdx.x & 31u;
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const Mat<double> g{ld_cs(in.g11 + i), ld_cs(in.g12 + i), ld_cs(in.g21 + i), ld_cs(in.g22 + i)};
+    Result<double> r;
+    bool bad = false;
+    fast::svd2_fast(g, r, bad);
+    store_result(out, i, r);
+    const unsigned active = __activemask();
+    const unsigned m = __ballot_sync(active, bad);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned base = 0;
+      if (static_cast<int>(lane) == leader) base = atomicAdd(count, static_cast<unsigned>(__popc(m)));
+      base = __shfl_sync(active, base, leader);
+      if (bad) list[base + __popc(m & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+    }
+  }
+}
+
+// the general algorithm over the deferred indices (gathered loads/stores)
+__global__ void __launch_bounds__(kThreads, 3)
+    k_svd2_list(InP<double> in, OutP<double> out, const uint32_t* list, const unsigned* count) {
+  const uint64_t cnt = *count;
+  for (uint64_t k = gtid(); k < cnt; k += gstride()) {
+    const uint64_t i = list[k];
+    const Mat<double> g{in.g11[i], in.g12[i], in.g21[i], in.g22[i]};
+    Result<double> r;
+    svd2<double>(g, opt_default(), r);
+    store_result(out, i, r);
+  }
+}
+
+// per-device deferred-index scratch (grown on demand; one per host thread so
+// concurrent callers on different threads never share it)
+struct Scratch {
+  uint32_t* list = nullptr;
+  unsigned* count = nullptr;
+  uint64_t cap = 0;
+};
+
+thread_local Scratch g_scratch[64];
+
+int scratch_for(uint64_t n, Scratch*& sc) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kog2_cuda_error("cudaGetDevice");
+  sc = &g_scratch[dev];
+  if (sc->cap >= n && sc->count) return KOG_OK;
+  if (sc->list) cudaFree(sc->list);
+  if (!sc->count && cudaMalloc(reinterpret_cast<void**>(&sc->count), sizeof(unsigned)) != cudaSuccess)
+    return kog2_cuda_error("cudaMalloc(defer count)");
+  if (cudaMalloc(reinterpret_cast<void**>(&sc->list), n * sizeof(uint32_t)) != cudaSuccess) {
+    sc->list = nullptr;
+    sc->cap = 0;
+    return kog2_cuda_error("cudaMalloc(defer list)");
+  }
+  sc->cap = n;
+  return KOG_OK;
+}
+
+constexpr uint64_t kFastChunk = 1ull << 31;  // uint32 deferred indices per launch pair
 
 template <class T, class MatC, class OutC>
 int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* opt, cudaStream_t st) {
@@ -60,25 +139,64 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
       !op.v11 || !op.v12 || !op.s || !op.flags)
     return kog2_arg_error("kog_svd2_batch: null array pointer");
   const Opt o = opt_of(opt);
+  static const bool general_only = std::getenv("KOG2_SVD2_GENERAL") != nullptr;  // A/B comparisons
+  if constexpr (sizeof(T) == 8) {
+    if (opt_is_default(o) && !general_only) {
+      Scratch* sc = nullptr;
+      int rc = scratch_for(n < kFastChunk ? n : kFastChunk, sc);
+      if (rc != KOG_OK) return rc;
+      for (uint64_t lo = 0; lo < n; lo += kFastChunk) {
+        const uint64_t len = n - lo < kFastChunk ? n - lo : kFastChunk;
+        const InP<T> ip{in->g11 + lo, in->g12 + lo, in->g21 + lo, in->g22 + lo};
+        const OutP<T> ol{op.sig1_f + lo, op.sig2_f + lo, op.sig1_e + lo, op.sig2_e + lo, op.u11 + lo,
+                         op.u12 + lo,    op.v11 + lo,    op.v12 + lo,    op.s + lo,      op.flags + lo};
+        if (cudaMemsetAsync(sc->count, 0, sizeof(unsigned), st) != cudaSuccess)
+          return kog2_cuda_error("cudaMemsetAsync(defer count)");
+        k_svd2_fast<<<grid_for(len), kThreads, 0, st>>>(ip, ol, len, sc->list, sc->count);
+        if ((rc = launched("k_svd2_fast")) != KOG_OK) return rc;
+        k_svd2_list<<<148 * 6, kThreads, 0, st>>>(ip, ol, sc->list, sc->count);
+        if ((rc = launched("k_svd2_list")) != KOG_OK) return rc;
+      }
+      return KOG_OK;
+    }
+  }
   const int grid = grid_for(n);
-  static const int minb = [] {  // occupancy variant (tuning knob, default 2)
-    const char* e = std::getenv("KOG2_SVD2_MINB");
-    return e ? std::atoi(e) : 3;
-  }();
-  if (!opt_is_default(o))
-    k_svd2<T, false, 2><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
-  else if (minb >= 4)
-    k_svd2<T, true, 4><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
-  else if (minb == 3)
-    k_svd2<T, true, 3><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
+  if (opt_is_default(o))
+    k_svd2<T, true><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
   else
-    k_svd2<T, true, 2><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
+    k_svd2<T, false><<<grid, kThreads, 0, st>>>(in_of<T>(in), op, n, o);
   return launched("k_svd2");
 }
 
 }  // namespace
 
 extern "C" {
+
+#ifdef KOG2_FAST_STATS
+// debug builds: per-reason counts of lanes that left the fast path (kog2_fast.cuh)
+// (out[0..15] = deferral reasons, out[16..23] = rare-path calls)
+int kog2_fast_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_kog2_fast_bad, sizeof(g_kog2_fast_bad)) != cudaSuccess ||
+      cudaMemcpyFromSymbol(out + KOG2_R_COUNT, g_kog2_rare, sizeof(g_kog2_rare)) != cudaSuccess)
+    return kog2_cuda_error("cudaMemcpyFromSymbol");
+  if (reset) {
+    const unsigned long long z[KOG2_R_COUNT] = {};
+    cudaMemcpyToSymbol(g_kog2_fast_bad, z, sizeof z);
+    cudaMemcpyToSymbol(g_kog2_rare, z, sizeof(g_kog2_rare));
+  }
+  return KOG_OK;
+}
+#endif
+
+int64_t kog_svd2_deferred_count(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
+  const Scratch* sc = &g_scratch[dev];
+  if (!sc->count) return -1;
+  unsigned c = 0;
+  if (cudaMemcpy(&c, sc->count, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return static_cast<int64_t>(c);
+}
 
 int kog_svd2_batch_f64(const kog_mat_f64* in, const kog_svd_out_f64* out, uint64_t n,
                        const kog_options* opt, void* stream) {
