@@ -114,7 +114,10 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 }
 
 template <class T, int ROUTINE>
-__global__ void __launch_bounds__(kThreads) k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt,
+#ifndef KOG2_STUDY_MINB
+#define KOG2_STUDY_MINB 3  // measured: 1 -> 111, 2 -> 111, 3 -> 120 M matrices/s (cfg5 rule, B200)
+#endif
+__global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB) k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt,
                                                     kog_stats* stats, BlockPartial* partial) {
   __shared__ unsigned cnt[19];
   __shared__ double red[5][kThreads / 32];

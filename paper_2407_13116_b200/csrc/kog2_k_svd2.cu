@@ -66,7 +66,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_svd2(InP<T> in, OutP<T> out, ui
 }
 
 // the specialised path; deferred indices go to list[0 .. *count)
-__global__ void __launch_bounds__(kThreads, 3)
+#ifndef KOG2_FAST_MINB
+#define KOG2_FAST_MINB 3
+#endif
+__global__ void __launch_bounds__(kThreads, KOG2_FAST_MINB)
     k_svd2_fast(InP<double> in, OutP<double> out, uint64_t n, uint32_t* list, unsigned* count) {
   const unsigned lane = threadIdx.x & 31u;
   for (uint64_t i = gtid(); i < n; i += gstride()) {
