@@ -32,8 +32,9 @@ static __device__ __noinline__ EPair<T> ep_make_rare(int ee, T ff) {
 __device__ __forceinline__ EPair<double> ep_make_(int ee, double ff, unsigned& err) {
   const int h = hiw(ff), e = bexp(h);
   if (normal_bexp(e)) return EPair<double>{ee + e - 1023, sethi(ff, (h & 0x800fffff) | 0x3ff00000)};
+  if (ff == 0.0) return EPair<double>{0, 0.0};  // canonical zero
   if (e == 0x7ff) err |= 1u;  // the reference throws on a NaN/inf mantissa
-  return ep_make_rare<double>(ee, ff);  // zero (canonical pair) or subnormal
+  return ep_make_rare<double>(ee, ff);  // subnormal
 }
 __device__ __forceinline__ EPair<float> ep_make_(int ee, float ff, unsigned& err) {
   const int b = __float_as_int(ff), e = bexpf(b);
