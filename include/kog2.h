@@ -39,6 +39,9 @@ extern "C" {
 
 const char* kog_last_error(void);
 const char* kog_version(void);
+/* Select the CUDA device for this host thread's subsequent calls (the library
+ * carries its own CUDA runtime; callers without one select devices here). */
+int kog_set_device(int device);
 
 /* ---------------------------------------------------------------- options */
 /* Options (svd2.hpp:122-132).  wide_channel: 0 = wider_type, 1 = kahan_det. */

@@ -19,6 +19,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 OBJDIR = os.path.join(ROOT, "build", "kog2")
 LIB = os.path.join(LIBDIR, "libkog2.so")
+BINDIR = os.path.join(HERE, "bin")
+CLI = os.path.join(BINDIR, "kog2_svd2batch")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 CUDA_HOME = os.path.dirname(os.path.dirname(os.path.realpath(NVCC)))
@@ -82,6 +84,12 @@ def build(force: bool = False, verbose: bool = False, variant: str | None = None
         list(ex.map(lambda j: _run(*j), jobs))
     if force or jobs or _newer(lib, objs):
         _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lpthread"])
+    if not variant:  # the svd2batch-compatible CLI, linked against the library (no CUDA runtime of its own)
+        os.makedirs(BINDIR, exist_ok=True)
+        cli_src = os.path.join(CSRC, "svd2batch.cpp")
+        if force or _newer(CLI, [cli_src, lib, os.path.join(ROOT, "include", "kog2.h")]):
+            _run(["g++", "-O2", "-std=c++17", f"-I{ROOT}/include", cli_src, "-o", CLI, f"-L{LIBDIR}", "-lkog2",
+                  "-Wl,-rpath,$ORIGIN/../lib"])
     if verbose:
         print("built", lib)
     return lib

@@ -131,6 +131,7 @@ i32 = C.c_int
 PROTOTYPES: dict[str, tuple] = {
     "kog_last_error": (C.c_char_p, []),
     "kog_version": (C.c_char_p, []),
+    "kog_set_device": (i32, [i32]),
     "kog_svd2_batch_f64": (i32, [PTR(kog_mat), PTR(kog_svd_out), u64, PTR(kog_options), P]),
     "kog_svd2_batch_f32": (i32, [PTR(kog_mat), PTR(kog_svd_out), u64, PTR(kog_options), P]),
     "kog_svd2_host_f64": (i32, [PTR(kog_mat), PTR(kog_svd_out), u64, PTR(kog_options)]),

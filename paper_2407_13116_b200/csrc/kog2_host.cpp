@@ -292,6 +292,11 @@ const char* kog_last_error(void) { return g_err.c_str(); }
 uint64_t kog_launch_count(void) { return g_launches.load(); }
 const char* kog_version(void) { return "kog2 0.1 (sm_100a)"; }
 
+int kog_set_device(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) return kog2_cuda_error("cudaSetDevice");
+  return KOG_OK;
+}
+
 int kog_svd2_host_f64(const kog_mat_f64* in, const kog_svd_out_f64* out, uint64_t n, const kog_options* opt) {
   return svd2_host<double>(in, out, n, opt, &kog_svd2_batch_f64);
 }
