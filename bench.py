@@ -364,7 +364,7 @@ def main() -> None:
                        "l2": "inputs (%.1f GiB per GPU) larger than the 126 MB L2" % (n * (bpm - (64 if suf == 'f64' else 40)) / 2**30)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk["source"],
-                         "kernel": "k_svd2", "bytes_per_matrix": bpm, "kernel_ms": kern_s * 1e3},
+                         "kernel": "k_svd2_fast + k_svd2_list (one kog_svd2_batch_f64 call)", "bytes_per_matrix": bpm, "kernel_ms": kern_s * 1e3},
             "e2e": e2e, "cpu_baseline": cpu, "study": study, "gpu_launches": launches,
             "clocks": clk.summary(), "fp64": fp64,
             "bit_exact": "outputs bit-identical to the reference (tests/test_gpu_parity.py)",

@@ -177,7 +177,7 @@ extern "C" {
 
 #ifdef KOG2_FAST_STATS
 // debug builds: per-reason counts of lanes that left the fast path (kog2_fast.cuh)
-// (out[0..15] = deferral reasons, out[16..23] = rare-path calls)
+// (out[0..15] = deferral reasons, out[16..31] = rare-path calls)
 int kog2_fast_stats(unsigned long long* out, int reset) {
   if (cudaMemcpyFromSymbol(out, g_kog2_fast_bad, sizeof(g_kog2_fast_bad)) != cudaSuccess ||
       cudaMemcpyFromSymbol(out + KOG2_R_COUNT, g_kog2_rare, sizeof(g_kog2_rare)) != cudaSuccess)

@@ -13,11 +13,12 @@ from paper_2407_13116_b200 import kogsvd2 as K  # noqa: E402
 NAMES = ["div", "hypot_arg", "hypot_ziv", "ep", "scal", "epval", "pattern", "subnormal_in", "s<0", "prescale",
          "t2p_equal", "general_inf", "oplus", "degenerate", "ilogb", "-",
          "rare:ilogb_sub", "rare:mant_sub", "rare:scalbn_slow", "rare:div_rare", "rare:hypot_rare", "rare:ep_make_rare",
-         "-", "-"]
+         "-", "-", "div:y0", "div:inf", "div:nan", "div:x0_ysub", "div:sub_operand", "div:sub_result", "-",
+         "div:x0_inline"]
 lib = capi.load()
 fn = lib.kog2_fast_stats
 fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-buf = (C.c_ulonglong * 24)()
+buf = (C.c_ulonglong * 32)()
 for k in (1, 2, 3):
     c = configs.cfg(k, count=1 << 22)
     g = K.generate(c, 0, c.count)
@@ -28,4 +29,4 @@ for k in (1, 2, 3):
     fn(buf, 1)
     d = lib.kog_svd2_deferred_count()
     print(f"cfg{k}: deferred {d / c.count:.4f}; events per matrix:",
-          {NAMES[i]: round(buf[i] / c.count, 4) for i in range(24) if buf[i]})
+          {NAMES[i]: round(buf[i] / c.count, 4) for i in range(32) if buf[i]})
