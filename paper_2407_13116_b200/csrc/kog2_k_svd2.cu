@@ -177,15 +177,18 @@ extern "C" {
 
 #ifdef KOG2_FAST_STATS
 // debug builds: per-reason counts of lanes that left the fast path (kog2_fast.cuh)
-// (out[0..15] = deferral reasons, out[16..31] = rare-path calls)
+// (out[0..15] = deferral reasons, out[16..31] = rare-path calls, out[32..95] = per-site division events)
 int kog2_fast_stats(unsigned long long* out, int reset) {
   if (cudaMemcpyFromSymbol(out, g_kog2_fast_bad, sizeof(g_kog2_fast_bad)) != cudaSuccess ||
       cudaMemcpyFromSymbol(out + KOG2_R_COUNT, g_kog2_rare, sizeof(g_kog2_rare)) != cudaSuccess)
     return kog2_cuda_error("cudaMemcpyFromSymbol");
+  if (cudaMemcpyFromSymbol(out + 32, kog2::fast::g_kog2_div_site, sizeof(kog2::fast::g_kog2_div_site)) != cudaSuccess)
+    return kog2_cuda_error("cudaMemcpyFromSymbol");
   if (reset) {
-    const unsigned long long z[KOG2_R_COUNT] = {};
-    cudaMemcpyToSymbol(g_kog2_fast_bad, z, sizeof z);
+    const unsigned long long z[64] = {};
+    cudaMemcpyToSymbol(g_kog2_fast_bad, z, sizeof(g_kog2_fast_bad));
     cudaMemcpyToSymbol(g_kog2_rare, z, sizeof(g_kog2_rare));
+    cudaMemcpyToSymbol(kog2::fast::g_kog2_div_site, z, sizeof(kog2::fast::g_kog2_div_site));
   }
   return KOG_OK;
 }

@@ -18,7 +18,7 @@ NAMES = ["div", "hypot_arg", "hypot_ziv", "ep", "scal", "epval", "pattern", "sub
 lib = capi.load()
 fn = lib.kog2_fast_stats
 fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-buf = (C.c_ulonglong * 32)()
+buf = (C.c_ulonglong * 96)()
 for k in (1, 2, 3):
     c = configs.cfg(k, count=1 << 22)
     g = K.generate(c, 0, c.count)
@@ -30,3 +30,5 @@ for k in (1, 2, 3):
     d = lib.kog_svd2_deferred_count()
     print(f"cfg{k}: deferred {d / c.count:.4f}; events per matrix:",
           {NAMES[i]: round(buf[i] / c.count, 4) for i in range(32) if buf[i]})
+    print("   div sites (zero numerator):", {i: round(buf[32 + i] / c.count, 4) for i in range(32) if buf[32 + i]})
+    print("   div sites (off fast path):", {i: round(buf[64 + i] / c.count, 4) for i in range(32) if buf[64 + i]})
