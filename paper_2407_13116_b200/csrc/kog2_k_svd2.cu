@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_svd2(InP<T> in, OutP<T> out, ui
 
 // the specialised path; deferred indices go to list[0 .. *count)
 #ifndef KOG2_FAST_MINB
-#define KOG2_FAST_MINB 3
+#define KOG2_FAST_MINB 4
 #endif
 __global__ void __launch_bounds__(kThreads, KOG2_FAST_MINB)
     k_svd2_fast(InP<double> in, OutP<double> out, uint64_t n, uint32_t* list, unsigned* count) {
