@@ -98,6 +98,38 @@ def test_hypot_exact_ties(cuda, dt):
 
 
 @pytest.mark.parametrize("dt", DTS)
+def test_hypot_near_the_early_out(cuda, ref, dt):
+    """Ratios small/big around kog2's widened early-out (2^-27 in double,
+    2^-12 in single): results equal the reference and the exact value, incl.
+    sec = hypot(t, 1) and big mantissas near 2 (largest relative half-ulp)."""
+    n = 400_000
+    rng = np.random.default_rng(0x68790003)
+    p = 53 if dt == np.float64 else 24
+    k = -np.arange(p // 2 - 8, p // 2 + 8)[rng.integers(0, 16, n)] if dt == np.float64 else \
+        -np.arange(4, 20)[rng.integers(0, 16, n)]
+    mb = np.where(rng.random(n) < 0.5, 2 - rng.random(n) * 2.0 ** -20, 1 + rng.random(n))
+    big = np.ldexp(mb, rng.integers(-60, 60, n))
+    small = big * np.ldexp(1 + rng.random(n), k)
+    a = big.astype(dt)
+    b = np.where(rng.random(n) < 0.25, np.ones(n), small).astype(dt)
+    a, b = np.where(rng.random(n) < 0.5, a, -a).astype(dt), b
+    sw = rng.random(n) < 0.5
+    a, b = np.where(sw, b, a).astype(dt), np.where(sw, a, b).astype(dt)
+    got = host(K.hypot_cr(dev(a), dev(b)))
+    want = np.empty_like(a)
+    (ref.hypot_f64 if dt == np.float64 else ref.hypot_f32)(a.ctypes.data, b.ctypes.data, want.ctypes.data, n)
+    _gen.assert_bits_equal(got, want, "hypot near the early-out")
+    ex = np.array([_gen.hypot_exact(x, y, dt) for x, y in zip(a[:20000], b[:20000])], dtype=dt)
+    _gen.assert_bits_equal(got[:20000], ex, "hypot near the early-out vs exact")
+    t = np.ldexp(1 + rng.random(n), -np.arange(10, 40)[rng.integers(0, 30, n)]).astype(dt)
+    sec = host(K.sec_from_tan(dev(t)))
+    want = np.empty_like(t)
+    one = np.ones_like(t)
+    (ref.hypot_f64 if dt == np.float64 else ref.hypot_f32)(t.ctypes.data, one.ctypes.data, want.ctypes.data, n)
+    _gen.assert_bits_equal(sec, want, "sec near the early-out")
+
+
+@pytest.mark.parametrize("dt", DTS)
 def test_hypot_adversarial_edges(cuda, ref, dt):
     """fpcore_test.cpp:75-89 plus inf/NaN conventions (fpcore.hpp:142-143)."""
     fi = np.finfo(dt)
