@@ -100,46 +100,23 @@ __device__ __forceinline__ float sgnmul(int s, float x) {
   return __int_as_float(__float_as_int(x) ^ (s & 0x80000000));
 }
 
-// apply_left (svd2.hpp:50-67): s * g, error-free
+// apply_left (svd2.hpp:50-67): s * g, error-free.  Each row of s has one
+// nonzero (+-1) entry: the source row and sign are selected, not branched on.
 template <class T>
 __device__ __forceinline__ Mat<T> apply_left(const SP& s, const Mat<T>& g) {
-  Mat<T> r;
-  if (s.m00 != 0) {
-    r.g11 = sgnmul(s.m00, g.g11);
-    r.g12 = sgnmul(s.m00, g.g12);
-  } else {
-    r.g11 = sgnmul(s.m01, g.g21);
-    r.g12 = sgnmul(s.m01, g.g22);
-  }
-  if (s.m10 != 0) {
-    r.g21 = sgnmul(s.m10, g.g11);
-    r.g22 = sgnmul(s.m10, g.g12);
-  } else {
-    r.g21 = sgnmul(s.m11, g.g21);
-    r.g22 = sgnmul(s.m11, g.g22);
-  }
-  return r;
+  const bool a0 = s.m00 != 0, a1 = s.m10 != 0;
+  const int k0 = a0 ? s.m00 : s.m01, k1 = a1 ? s.m10 : s.m11;
+  return Mat<T>{sgnmul(k0, a0 ? g.g11 : g.g21), sgnmul(k0, a0 ? g.g12 : g.g22), sgnmul(k1, a1 ? g.g11 : g.g21),
+                sgnmul(k1, a1 ? g.g12 : g.g22)};
 }
 
-// apply_right (svd2.hpp:69-86): g * s, error-free
+// apply_right (svd2.hpp:69-86): g * s, error-free (source column selected)
 template <class T>
 __device__ __forceinline__ Mat<T> apply_right(const Mat<T>& g, const SP& s) {
-  Mat<T> r;
-  if (s.m00 != 0) {
-    r.g11 = sgnmul(s.m00, g.g11);
-    r.g21 = sgnmul(s.m00, g.g21);
-  } else {
-    r.g11 = sgnmul(s.m10, g.g12);
-    r.g21 = sgnmul(s.m10, g.g22);
-  }
-  if (s.m01 != 0) {
-    r.g12 = sgnmul(s.m01, g.g11);
-    r.g22 = sgnmul(s.m01, g.g21);
-  } else {
-    r.g12 = sgnmul(s.m11, g.g12);
-    r.g22 = sgnmul(s.m11, g.g22);
-  }
-  return r;
+  const bool a0 = s.m00 != 0, a1 = s.m01 != 0;
+  const int k0 = a0 ? s.m00 : s.m10, k1 = a1 ? s.m01 : s.m11;
+  return Mat<T>{sgnmul(k0, a0 ? g.g11 : g.g12), sgnmul(k1, a1 ? g.g11 : g.g12), sgnmul(k0, a0 ? g.g21 : g.g22),
+                sgnmul(k1, a1 ? g.g21 : g.g22)};
 }
 
 // Options (svd2.hpp:122-132).  Kernels pass either a compile-time constant
