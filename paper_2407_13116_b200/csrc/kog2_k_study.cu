@@ -39,7 +39,7 @@ __global__ void k_svd2_ext(InP<T> in, kog_extsvd* o, uint64_t n) {
 template <class T>
 __device__ __forceinline__ uint32_t run_one_kog(const Mat<T>& g, const Opt& o, Metrics& m) {
   ExtSvd ref;
-  svd2_ext(g, ref);
+  svd2_ext<T, false>(g, ref);  // metrics() reads the singular values only
   Result<T> r;
   svd2<T>(g, o, r);
   uint32_t flags = r.flags;
@@ -53,7 +53,7 @@ __device__ __forceinline__ uint32_t run_one_kog(const Mat<T>& g, const Opt& o, M
 template <class T>
 __device__ __forceinline__ uint32_t run_one_lasv2(const Mat<T>& g, Metrics& m) {
   ExtSvd ref;
-  svd2_ext(g, ref);
+  svd2_ext<T, false>(g, ref);  // metrics() reads the singular values only
   const Lasv2<T> r = lasv2(g.g11, g.g12, g.g22);
   const Mat<T> u{r.csl, -r.snl, r.snl, r.csl};
   const Mat<T> v{r.csr, -r.snr, r.snr, r.csr};
