@@ -50,6 +50,36 @@ __device__ __forceinline__ uint32_t run_one_kog(const Mat<T>& g, const Opt& o, M
   return flags;
 }
 
+// the decomposition as kog_svd2_batch stored it (compact SoA, include/kog2.h)
+template <class T>
+struct SvdBuf {
+  const T *sig1_f, *sig2_f;
+  const int32_t *sig1_e, *sig2_e;
+  const T *u11, *u12, *v11, *v12;
+  const uint32_t* flags;
+};
+
+__device__ __forceinline__ double with_sign(double mag, bool neg) { return neg ? -mag : mag; }
+__device__ __forceinline__ float with_sign(float mag, bool neg) { return neg ? -mag : mag; }
+
+// run_one (harness.hpp:190-222) on a decomposition computed by the svd2
+// kernels: U and V are expanded exactly (|u22| = |u11|, |u21| = |u12| with the
+// stored signs), so the metrics see the reference's own factors
+template <class T>
+__device__ __forceinline__ uint32_t run_one_buf(const Mat<T>& g, const SvdBuf<T>& b, uint64_t i, Metrics& m) {
+  ExtSvd ref;
+  svd2_ext<T, false>(g, ref);  // metrics() reads the singular values only
+  uint32_t flags = b.flags[i];
+  const T u11 = b.u11[i], u12 = b.u12[i], v11 = b.v11[i], v12 = b.v12[i];
+  const Mat<T> u{u11, u12, with_sign(fabs(u12), flags & KOG_F_SIGN_U21), with_sign(fabs(u11), flags & KOG_F_SIGN_U22)};
+  const Mat<T> v{v11, v12, with_sign(fabs(v12), flags & KOG_F_SIGN_V21), with_sign(fabs(v11), flags & KOG_F_SIGN_V22)};
+  const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
+  if (!all_finite(u) || !all_finite(v) || !is_finite(s1.f) || !is_finite(s2.f)) flags |= KOG_M_NONFINITE_FACTOR;
+  metrics(g, u, v, ext_from_pair(s1), ext_from_pair(s2), ref, m);
+  if (isnan(m.reG) || isnan(m.reS1) || isnan(m.reS2) || isnan(m.reU) || isnan(m.reV)) flags |= KOG_M_NAN_METRIC;
+  return flags;
+}
+
 template <class T>
 __device__ __forceinline__ uint32_t run_one_lasv2(const Mat<T>& g, Metrics& m) {
   ExtSvd ref;
@@ -113,12 +143,13 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
 }
 
-template <class T, int ROUTINE>
+template <class T, int ROUTINE, bool PHASED>
 #ifndef KOG2_STUDY_MINB
 #define KOG2_STUDY_MINB 3  // measured: 1 -> 111, 2 -> 111, 3 -> 120 M matrices/s (cfg5 rule, B200)
 #endif
-__global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB) k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt,
-                                                    kog_stats* stats, BlockPartial* partial) {
+__global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB)
+    k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt, kog_stats* stats, BlockPartial* partial, InP<T> gin,
+            SvdBuf<T> sb) {
   __shared__ unsigned cnt[19];
   __shared__ double red[5][kThreads / 32];
   __shared__ Ext kred_k[kThreads / 32];
@@ -135,13 +166,17 @@ __global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB) k_study(GenCfg c, u
 
   for (uint64_t i = gtid(); i < n; i += gstride()) {
     const unsigned long long index = index0 + i;
-    const Mat<T> g = generate<T>(c, index);
     Metrics m;
     uint32_t flags;
-    if (ROUTINE == KOG_ROUTINE_KOG)
-      flags = run_one_kog<T>(g, opt, m);
-    else
-      flags = run_one_lasv2<T>(g, m);
+    if constexpr (PHASED) {  // generated and decomposed by the earlier launches of this chunk
+      flags = run_one_buf<T>(load_mat(gin, i), sb, i, m);
+    } else {
+      const Mat<T> g = generate<T>(c, index);
+      if (ROUTINE == KOG_ROUTINE_KOG)
+        flags = run_one_kog<T>(g, opt, m);
+      else
+        flags = run_one_lasv2<T>(g, m);
+    }
     bool ok = true;
     if (flags & KOG_M_NONFINITE_FACTOR) {
       ok = false;
@@ -321,6 +356,100 @@ int launch_ext(const MatC* g, kog_extsvd* o, uint64_t n, cudaStream_t st) {
   return launched("k_svd2_ext");
 }
 
+
+// ------------------------------------------------------------ study launcher
+// Per device and host thread: the per-block (kappa, index) slots and, for the
+// phased kog study, one chunk of generated matrices and their decompositions.
+struct StudyScratch {
+  BlockPartial* part = nullptr;
+  int blocks = 0;
+  void* buf = nullptr;
+  size_t cap = 0;
+};
+thread_local StudyScratch g_study[64];
+
+int study_grid(uint64_t n, int sms) {
+  uint64_t want = (n + kThreads - 1) / kThreads;
+  const uint64_t cap = static_cast<uint64_t>(sms) * 8ull;
+  return static_cast<int>(want > cap ? cap : want);
+}
+
+int study_partials(StudyScratch& sc, int grid) {
+  if (sc.blocks >= grid) return KOG_OK;
+  if (sc.part) cudaFree(sc.part);
+  sc.part = nullptr;
+  sc.blocks = 0;
+  if (cudaMalloc(reinterpret_cast<void**>(&sc.part), sizeof(BlockPartial) * grid) != cudaSuccess)
+    return kog2_cuda_error("cudaMalloc(study partials)");
+  sc.blocks = grid;
+  return KOG_OK;
+}
+
+constexpr uint64_t kStudyChunk = 1ull << 22;
+
+template <class T> struct Abi;
+template <> struct Abi<double> {
+  using Mat = kog_mat_f64;
+  using Out = kog_svd_out_f64;
+  static int gen(const kog_run_config* c, uint64_t i0, const Mat* m, uint64_t n, void* st) {
+    return kog_generate_batch_f64(c, i0, m, n, st);
+  }
+  static int svd(const Mat* m, const Out* o, uint64_t n, const kog_options* opt, void* st) {
+    return kog_svd2_batch_f64(m, o, n, opt, st);
+  }
+};
+template <> struct Abi<float> {
+  using Mat = kog_mat_f32;
+  using Out = kog_svd_out_f32;
+  static int gen(const kog_run_config* c, uint64_t i0, const Mat* m, uint64_t n, void* st) {
+    return kog_generate_batch_f32(c, i0, m, n, st);
+  }
+  static int svd(const Mat* m, const Out* o, uint64_t n, const kog_options* opt, void* st) {
+    return kog_svd2_batch_f32(m, o, n, opt, st);
+  }
+};
+
+// The kog study in phases per chunk — generate, the svd2 kernels (the
+// specialised fast path where the Options allow), then the reference
+// singular values + metrics + ErrorStats from the buffers.  Each launch runs
+// a fraction of the fused kernel's code (the fused kernel was bound by
+// instruction fetch: ~85% "no instruction" stalls), and the buffers cost
+// ~200 B of HBM traffic per matrix.
+template <class T>
+int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats, StudyScratch& sc, int sms,
+                 cudaStream_t st) {
+  const uint64_t C = n < kStudyChunk ? n : kStudyChunk;
+  const size_t need = static_cast<size_t>(C) * (10 * sizeof(T) + 4 * sizeof(int32_t));
+  if (sc.cap < need) {
+    if (sc.buf) cudaFree(sc.buf);
+    sc.buf = nullptr;
+    sc.cap = 0;
+    if (cudaMalloc(&sc.buf, need) != cudaSuccess) return kog2_cuda_error("cudaMalloc(study chunk)");
+    sc.cap = need;
+  }
+  T* t = static_cast<T*>(sc.buf);
+  int32_t* w = reinterpret_cast<int32_t*>(t + 10 * C);
+  const typename Abi<T>::Mat gm{t, t + C, t + 2 * C, t + 3 * C};
+  const typename Abi<T>::Out om{t + 4 * C, t + 5 * C, w,         w + C,     t + 6 * C,
+                                t + 7 * C, t + 8 * C, t + 9 * C, w + 2 * C, reinterpret_cast<uint32_t*>(w + 3 * C)};
+  const InP<T> gin{t, t + C, t + 2 * C, t + 3 * C};
+  const SvdBuf<T> sb{om.sig1_f, om.sig2_f, om.sig1_e, om.sig2_e, om.u11, om.u12, om.v11, om.v12, om.flags};
+  int rc = study_partials(sc, study_grid(C, sms));
+  if (rc != KOG_OK) return rc;
+  for (uint64_t lo = 0; lo < n; lo += C) {
+    const uint64_t len = n - lo < C ? n - lo : C;
+    if ((rc = Abi<T>::gen(cfg, index0 + lo, &gm, len, st)) != KOG_OK) return rc;
+    if ((rc = Abi<T>::svd(&gm, &om, len, &cfg->options, st)) != KOG_OK) return rc;
+    const int grid = study_grid(len, sms);
+    k_study<T, KOG_ROUTINE_KOG, true><<<grid, kThreads, 0, st>>>(GenCfg{}, index0 + lo, len, Opt{}, stats, sc.part,
+                                                                  gin, sb);
+    if ((rc = launched("k_study")) != KOG_OK) return rc;
+    k_study_finish<<<1, kThreads, 0, st>>>(stats, sc.part, grid);
+    if ((rc = launched("k_study_finish")) != KOG_OK) return rc;
+  }
+  return KOG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -361,42 +490,28 @@ int kog_study_batch(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_
   if (!cfg || !stats_dev) return kog2_arg_error("kog_study_batch: null argument");
   if (kog_validate(cfg) != KOG_OK) return KOG_ERR_ARG;
   if (n == 0) return KOG_OK;
-  // per-block (kappa, index) slots: a lazily grown per-thread, per-device scratch
-  static thread_local BlockPartial* scratch[64] = {};
-  static thread_local int scratch_blocks[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kog2_cuda_error("cudaGetDevice");
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  uint64_t want = (n + kThreads - 1) / kThreads;
-  const uint64_t cap = static_cast<uint64_t>(sms) * 8ull;
-  if (want > cap) want = cap;
-  const int grid = static_cast<int>(want);
-  if (scratch_blocks[dev] < grid) {
-    if (scratch[dev]) cudaFree(scratch[dev]);
-    scratch[dev] = nullptr;
-    if (cudaMalloc(reinterpret_cast<void**>(&scratch[dev]), sizeof(BlockPartial) * grid) != cudaSuccess)
-      return kog2_cuda_error("cudaMalloc(study scratch)");
-    scratch_blocks[dev] = grid;
-  }
+  StudyScratch& sc = g_study[dev];
+  cudaStream_t st = KOG2_ST(stream);
+  if (cfg->routine == KOG_ROUTINE_KOG)
+    return cfg->single_precision ? study_phased<float>(cfg, index0, n, stats_dev, sc, sms, st)
+                                 : study_phased<double>(cfg, index0, n, stats_dev, sc, sms, st);
+  const int grid = study_grid(n, sms);
+  int rc = study_partials(sc, grid);
+  if (rc != KOG_OK) return rc;
   const GenCfg g = gen_cfg_of(cfg);
   const Opt o = opt_of(&cfg->options);
-  cudaStream_t st = KOG2_ST(stream);
-  BlockPartial* part = scratch[dev];
-  if (cfg->single_precision) {
-    if (cfg->routine == KOG_ROUTINE_LASV2)
-      k_study<float, KOG_ROUTINE_LASV2><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, part);
-    else
-      k_study<float, KOG_ROUTINE_KOG><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, part);
-  } else {
-    if (cfg->routine == KOG_ROUTINE_LASV2)
-      k_study<double, KOG_ROUTINE_LASV2><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, part);
-    else
-      k_study<double, KOG_ROUTINE_KOG><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, part);
-  }
-  const int rc = launched("k_study");
-  if (rc != KOG_OK) return rc;
-  k_study_finish<<<1, kThreads, 0, st>>>(stats_dev, part, grid);
+  if (cfg->single_precision)
+    k_study<float, KOG_ROUTINE_LASV2, false><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, sc.part, InP<float>{},
+                                                                         SvdBuf<float>{});
+  else
+    k_study<double, KOG_ROUTINE_LASV2, false><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, sc.part,
+                                                                          InP<double>{}, SvdBuf<double>{});
+  if ((rc = launched("k_study")) != KOG_OK) return rc;
+  k_study_finish<<<1, kThreads, 0, st>>>(stats_dev, sc.part, grid);
   return launched("k_study_finish");
 }
 
