@@ -51,13 +51,31 @@ __device__ __forceinline__ uint32_t run_one_kog(const Mat<T>& g, const Opt& o, M
 }
 
 // the decomposition as kog_svd2_batch stored it (compact SoA, include/kog2.h)
+// and the reference singular values (k_ref_sigma)
 template <class T>
 struct SvdBuf {
   const T *sig1_f, *sig2_f;
   const int32_t *sig1_e, *sig2_e;
   const T *u11, *u12, *v11, *v12;
   const uint32_t* flags;
+  long long *re1, *re2;
+  double *rh1, *rl1, *rh2, *rl2;
 };
+
+// svd2_ext's singular values (oracle.hpp:102-238) of a chunk, SoA
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_ref_sigma(InP<T> in, SvdBuf<T> b, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    ExtSvd ref;
+    svd2_ext<T, false>(load_mat(in, i), ref);
+    b.re1[i] = ref.sigma1.e;
+    b.rh1[i] = ref.sigma1.hi;
+    b.rl1[i] = ref.sigma1.lo;
+    b.re2[i] = ref.sigma2.e;
+    b.rh2[i] = ref.sigma2.hi;
+    b.rl2[i] = ref.sigma2.lo;
+  }
+}
 
 __device__ __forceinline__ double with_sign(double mag, bool neg) { return neg ? -mag : mag; }
 __device__ __forceinline__ float with_sign(float mag, bool neg) { return neg ? -mag : mag; }
@@ -67,8 +85,9 @@ __device__ __forceinline__ float with_sign(float mag, bool neg) { return neg ? -
 // stored signs), so the metrics see the reference's own factors
 template <class T>
 __device__ __forceinline__ uint32_t run_one_buf(const Mat<T>& g, const SvdBuf<T>& b, uint64_t i, Metrics& m) {
-  ExtSvd ref;
-  svd2_ext<T, false>(g, ref);  // metrics() reads the singular values only
+  ExtSvd ref;  // metrics() reads the singular values only
+  ref.sigma1 = Ext{b.re1[i], b.rh1[i], b.rl1[i]};
+  ref.sigma2 = Ext{b.re2[i], b.rh2[i], b.rl2[i]};
   uint32_t flags = b.flags[i];
   const T u11 = b.u11[i], u12 = b.u12[i], v11 = b.v11[i], v12 = b.v12[i];
   const Mat<T> u{u11, u12, with_sign(fabs(u12), flags & KOG_F_SIGN_U21), with_sign(fabs(u11), flags & KOG_F_SIGN_U22)};
@@ -419,7 +438,7 @@ template <class T>
 int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats, StudyScratch& sc, int sms,
                  cudaStream_t st) {
   const uint64_t C = n < kStudyChunk ? n : kStudyChunk;
-  const size_t need = static_cast<size_t>(C) * (10 * sizeof(T) + 4 * sizeof(int32_t));
+  const size_t need = static_cast<size_t>(C) * (6 * 8 + 10 * sizeof(T) + 4 * sizeof(int32_t));
   if (sc.cap < need) {
     if (sc.buf) cudaFree(sc.buf);
     sc.buf = nullptr;
@@ -427,19 +446,24 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
     if (cudaMalloc(&sc.buf, need) != cudaSuccess) return kog2_cuda_error("cudaMalloc(study chunk)");
     sc.cap = need;
   }
-  T* t = static_cast<T*>(sc.buf);
+  double* rd = static_cast<double*>(sc.buf);  // the 8-byte reference arrays first (alignment)
+  long long* rq = reinterpret_cast<long long*>(rd);
+  T* t = reinterpret_cast<T*>(rd + 6 * C);
   int32_t* w = reinterpret_cast<int32_t*>(t + 10 * C);
   const typename Abi<T>::Mat gm{t, t + C, t + 2 * C, t + 3 * C};
   const typename Abi<T>::Out om{t + 4 * C, t + 5 * C, w,         w + C,     t + 6 * C,
                                 t + 7 * C, t + 8 * C, t + 9 * C, w + 2 * C, reinterpret_cast<uint32_t*>(w + 3 * C)};
   const InP<T> gin{t, t + C, t + 2 * C, t + 3 * C};
-  const SvdBuf<T> sb{om.sig1_f, om.sig2_f, om.sig1_e, om.sig2_e, om.u11, om.u12, om.v11, om.v12, om.flags};
+  const SvdBuf<T> sb{om.sig1_f, om.sig2_f, om.sig1_e, om.sig2_e, om.u11, om.u12, om.v11,
+                     om.v12,    om.flags,  rq,        rq + C,    rd + 2 * C, rd + 3 * C, rd + 4 * C, rd + 5 * C};
   int rc = study_partials(sc, study_grid(C, sms));
   if (rc != KOG_OK) return rc;
   for (uint64_t lo = 0; lo < n; lo += C) {
     const uint64_t len = n - lo < C ? n - lo : C;
     if ((rc = Abi<T>::gen(cfg, index0 + lo, &gm, len, st)) != KOG_OK) return rc;
     if ((rc = Abi<T>::svd(&gm, &om, len, &cfg->options, st)) != KOG_OK) return rc;
+    k_ref_sigma<T><<<grid_for(len), kThreads, 0, st>>>(gin, sb, len);
+    if ((rc = launched("k_ref_sigma")) != KOG_OK) return rc;
     const int grid = study_grid(len, sms);
     k_study<T, KOG_ROUTINE_KOG, true><<<grid, kThreads, 0, st>>>(GenCfg{}, index0 + lo, len, Opt{}, stats, sc.part,
                                                                   gin, sb);
