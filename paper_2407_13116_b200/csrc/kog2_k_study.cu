@@ -64,7 +64,10 @@ struct SvdBuf {
 
 // svd2_ext's singular values (oracle.hpp:102-238) of a chunk, SoA
 template <class T>
-__global__ void __launch_bounds__(kThreads) k_ref_sigma(InP<T> in, SvdBuf<T> b, uint64_t n) {
+#ifndef KOG2_REF_MINB
+#define KOG2_REF_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, KOG2_REF_MINB) k_ref_sigma(InP<T> in, SvdBuf<T> b, uint64_t n) {
   for (uint64_t i = gtid(); i < n; i += gstride()) {
     ExtSvd ref;
     svd2_ext<T, false>(load_mat(in, i), ref);
@@ -164,7 +167,7 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 
 template <class T, int ROUTINE, bool PHASED>
 #ifndef KOG2_STUDY_MINB
-#define KOG2_STUDY_MINB 3  // measured: 1 -> 111, 2 -> 111, 3 -> 120 M matrices/s (cfg5 rule, B200)
+#define KOG2_STUDY_MINB 4  // measured (phased, cfg5 rule): 2 -> 950, 3 -> 980, 4 -> 1010 M matrices/s
 #endif
 __global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB)
     k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt, kog_stats* stats, BlockPartial* partial, InP<T> gin,
