@@ -240,11 +240,13 @@ def main() -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())  # identity on an N-GPU box
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # nccl (one rank per GPU); KOG2_BENCH_BACKEND=gloo only for functional checks of the N>1 flow
+        backend = os.environ.get("KOG2_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
 
     def barrier():
         if world > 1:
@@ -327,9 +329,12 @@ def main() -> None:
     # ---- end to end through the public host-buffer API (pinned host memory)
     e2e = None
     if not args.no_e2e:
-        gh = torch.empty((4, n), dtype=g.dtype, pin_memory=True)
-        gh.copy_(g)
-        oh = {k: torch.empty_like(v, device="cpu", pin_memory=True) for k, v in out.items()}
+        # host batch: the rank's whole shard at N=1; at N>1 the first 2^26 matrices of it per rank (bounds the
+        # pinned host memory to 6 GiB per rank; the rate is a steady-state pipeline rate either way)
+        ne = n if world == 1 else min(n, 1 << 26)
+        gh = torch.empty((4, ne), dtype=g.dtype, pin_memory=True)
+        gh.copy_(g[:, :ne])
+        oh = {k: torch.empty(ne, dtype=v.dtype, pin_memory=True) for k, v in out.items()}
         del out
         torch.cuda.empty_cache()
         K.svd2_host(gh, out=oh)  # warm-up (pipeline buffers)
@@ -339,8 +344,8 @@ def main() -> None:
         for _ in range(steps):
             K.svd2_host(gh, out=oh)
         dt = max_over_ranks((time.perf_counter() - t0) / steps)
-        e2e = {"value": world * n / dt, "unit": UNIT, "h2d_bytes_per_step": world * n * (bpm - (64 if suf == "f64" else 40)),
-               "d2h_bytes_per_step": world * n * (64 if suf == "f64" else 40),
+        e2e = {"value": world * ne / dt, "unit": UNIT, "h2d_bytes_per_step": world * ne * (bpm - (64 if suf == "f64" else 40)),
+               "d2h_bytes_per_step": world * ne * (64 if suf == "f64" else 40), "matrices_per_step": world * ne,
                "api": "kog_svd2_host_f64 (pinned host buffers, chunked H2D/kernel/D2H pipeline)"}
         g_host = gh.numpy()
     else:
@@ -358,7 +363,7 @@ def main() -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": suf,
             "data": "synthetic (seeded on-device counter-based generator, SURVEY.md §8d)",
             "config": {"workload": f"cfg{args.config}: {n} general {suf} 2x2 matrices per GPU"
-                                   + (" (e in [-500,500], 1/8 zero patterns); rank r owns indices [r*2^28,(r+1)*2^28) of config 5" if args.config == 3 else ""),
+                                   + (f" (e in [-500,500], 1/8 zero patterns); rank r owns indices [r*{n},(r+1)*{n}) of config 5" if args.config == 3 else ""),
                        "model": "enhanced 2x2 Kogbetliantz svd2 (arXiv 2407.13116)", "global_batch": world * n,
                        "parallelism": f"dp{world} (index-range shards, no data-path collective)",
                        "l2": "inputs (%.1f GiB per GPU) larger than the 126 MB L2" % (n * (bpm - (64 if suf == 'f64' else 40)) / 2**30)},
