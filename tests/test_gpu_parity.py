@@ -466,7 +466,14 @@ def test_run_batch_vs_reference_counts(cuda, ref):
                 K.RunConfig(shape=capi.SHAPE_TRI, regime=capi.REGIME_CIRC, count=1 << 18, seed=78),
                 K.RunConfig(shape=capi.SHAPE_TRI, regime=capi.REGIME_BULLET, count=50000, seed=0x1234ABCD,
                             routine=capi.ROUTINE_LASV2),
-                configs.cfg(3, count=1 << 18), configs.cfg(4, count=1 << 18), configs.cfg(2, count=1 << 18)):
+                configs.cfg(3, count=1 << 18), configs.cfg(4, count=1 << 18), configs.cfg(2, count=1 << 18),
+                # more than one 2^22-matrix chunk of the phased study
+                configs.cfg(5, count=(1 << 22) + 4099),
+                # non-default Options: the general svd2 kernel inside the study
+                K.RunConfig(shape=capi.SHAPE_GEN, regime=capi.REGIME_BULLET, count=1 << 17, seed=79,
+                            options=K.Options(hypot_is_cr=False, ominus_for_d=True)),
+                K.RunConfig(single_precision=True, shape=capi.SHAPE_GEN, regime=capi.REGIME_BULLET, count=1 << 17,
+                            seed=80, options=K.Options(hypot_is_cr=False))):
         st = K.run_batch(cfg)
         rc, want, msg = refbind.run_batch(ref, cfg.c())
         assert rc == 0, msg
