@@ -36,11 +36,13 @@ __device__ __forceinline__ EPair<double> ep_make_(int ee, double ff, unsigned& e
   if (e == 0x7ff) err |= 1u;  // the reference throws on a NaN/inf mantissa
   return ep_make_rare<double>(ee, ff);  // subnormal
 }
+// binary32: through the (always normal) double, without branches for zero and
+// subnormal mantissas; NaN/inf set err (the reference throws)
 __device__ __forceinline__ EPair<float> ep_make_(int ee, float ff, unsigned& err) {
-  const int b = __float_as_int(ff), e = bexpf(b);
-  if (normal_bexpf(e)) return EPair<float>{ee + e - 127, __int_as_float((b & 0x807fffff) | 0x3f800000)};
-  if (e == 0xff) err |= 1u;
-  return ep_make_rare<float>(ee, ff);
+  const int b = __float_as_int(ff);
+  if (bexpf(b) == 0xff) err |= 1u;
+  const bool z = (b & 0x7fffffff) == 0 || bexpf(b) == 0xff;
+  return z ? EPair<float>{0, 0.0f} : EPair<float>{ee + ilogb_nz(ff), mant_nz(ff)};
 }
 template <class T>
 __device__ __forceinline__ EPair<T> ep_make(int ee, T ff, unsigned& err) {
