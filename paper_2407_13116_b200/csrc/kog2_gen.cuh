@@ -26,39 +26,55 @@ struct Stream {
   }
 };
 
-// u % m (the reference's 64-bit modulo, harness.hpp:152)
-__device__ __forceinline__ unsigned long long umod_small(unsigned long long u, unsigned long long m) {
-  return u % m;
+// u % m, the reference's 64-bit modulo (harness.hpp:152), without a 64-bit
+// division: with M = floor((2^64 - 1) / m) (precomputed on the host),
+// 2^64/m - 1 <= M < 2^64/m, so q~ = floor(u M / 2^64) is floor(u/m) or one
+// less and u - q~ m lies in [0, 2m): one conditional subtraction is exact
+struct UMod {
+  unsigned long long m, magic;
+};
+inline UMod umod_of(unsigned long long m) { return UMod{m, m ? ~0ull / m : 0ull}; }
+__device__ __forceinline__ unsigned long long umod(unsigned long long u, const UMod& d) {
+  const unsigned long long r = u - __umul64hi(u, d.magic) * d.m;
+  return r >= d.m ? r - d.m : r;
 }
 
-// POD mirror of the generator fields of kog_run_config, passed by value
+// POD mirror of the generator fields of kog_run_config, passed by value, with
+// the ranged draw's exponent window resolved for T (harness.hpp:157-166)
 struct GenCfg {
   unsigned long long seed;
-  int shape, regime, varsigma;
-  int elo, ehi, tail_lo, tail_hi;
-  unsigned tail_mod, zero_mask_rule;
+  int shape, regime;
+  int lo, hi;  // bullet [e_mu, e_nu - 2], sigma [e_mu + varsigma, e_nu - 2], ranged [elo, ehi]
+  UMod range;  // hi - lo + 1
+  int tail_lo, tail_hi;
+  UMod tail_range, tail_mod;
+  unsigned zero_mask_rule;
 };
 
+template <class T>
 inline GenCfg gen_cfg_of(const kog_run_config* c) {
   GenCfg g;
   g.seed = c->seed;
   g.shape = c->shape;
   g.regime = c->regime;
-  g.varsigma = c->varsigma;
-  g.elo = c->elo;
-  g.ehi = c->ehi;
+  g.lo = c->regime == KOG_REGIME_BULLET  ? FP<T>::emin
+         : c->regime == KOG_REGIME_SIGMA ? FP<T>::emin + c->varsigma
+                                         : c->elo;
+  g.hi = c->regime == KOG_REGIME_RANGED ? c->ehi : FP<T>::emax - 2;
+  g.range = umod_of(static_cast<unsigned long long>(g.hi - g.lo + 1));
   g.tail_lo = c->tail_lo;
   g.tail_hi = c->tail_hi;
-  g.tail_mod = c->tail_mod;
+  g.tail_range = umod_of(static_cast<unsigned long long>(c->tail_hi - c->tail_lo + 1));
+  g.tail_mod = umod_of(c->tail_mod);
   g.zero_mask_rule = c->zero_mask_rule;
   return g;
 }
 
 template <class T>
-__device__ __forceinline__ T gen_ranged(Stream& st, int elo, int ehi) {  // harness.hpp:150-156
+__device__ __forceinline__ T gen_ranged(Stream& st, int elo, const UMod& range) {  // harness.hpp:150-156
   constexpr int p = FP<T>::p;
   const unsigned long long u = st.next();
-  const int e = elo + static_cast<int>(umod_small(u, static_cast<unsigned long long>(ehi - elo + 1)));
+  const int e = elo + static_cast<int>(umod(u, range));
   const T f = T(1) + scalbn_t(static_cast<T>(st.next() >> (64 - (p - 1))), 1 - p);
   const T v = scalbn_t(f, e);
   return (u >> 63) ? -v : v;
@@ -73,20 +89,12 @@ __device__ __forceinline__ T gen_circ(Stream& st) {  // harness.hpp:145-149
 
 template <class T>
 __device__ __forceinline__ T gen_element(Stream& st, const GenCfg& c) {  // harness.hpp:157-166
-  switch (c.regime) {
-    case KOG_REGIME_CIRC:
-      return gen_circ<T>(st);
-    case KOG_REGIME_BULLET:
-      return gen_ranged<T>(st, FP<T>::emin, FP<T>::emax - 2);
-    case KOG_REGIME_SIGMA:
-      return gen_ranged<T>(st, FP<T>::emin + c.varsigma, FP<T>::emax - 2);
-    default:  // KOG_REGIME_RANGED
-      if (c.tail_mod != 0) {
-        const unsigned long long t = st.next();
-        if (umod_small(t, c.tail_mod) == 0) return gen_ranged<T>(st, c.tail_lo, c.tail_hi);
-      }
-      return gen_ranged<T>(st, c.elo, c.ehi);
+  if (c.regime == KOG_REGIME_CIRC) return gen_circ<T>(st);
+  if (c.regime == KOG_REGIME_RANGED && c.tail_mod.m != 0) {
+    const unsigned long long t = st.next();
+    if (umod(t, c.tail_mod) == 0) return gen_ranged<T>(st, c.tail_lo, c.tail_range);
   }
+  return gen_ranged<T>(st, c.lo, c.range);  // bullet, sigma, ranged
 }
 
 template <class T>

@@ -529,14 +529,13 @@ int kog_study_batch(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_
   const int grid = study_grid(n, sms);
   int rc = study_partials(sc, grid);
   if (rc != KOG_OK) return rc;
-  const GenCfg g = gen_cfg_of(cfg);
   const Opt o = opt_of(&cfg->options);
   if (cfg->single_precision)
-    k_study<float, KOG_ROUTINE_LASV2, false><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, sc.part, InP<float>{},
-                                                                         SvdBuf<float>{});
+    k_study<float, KOG_ROUTINE_LASV2, false><<<grid, kThreads, 0, st>>>(gen_cfg_of<float>(cfg), index0, n, o, stats_dev,
+                                                                         sc.part, InP<float>{}, SvdBuf<float>{});
   else
-    k_study<double, KOG_ROUTINE_LASV2, false><<<grid, kThreads, 0, st>>>(g, index0, n, o, stats_dev, sc.part,
-                                                                          InP<double>{}, SvdBuf<double>{});
+    k_study<double, KOG_ROUTINE_LASV2, false><<<grid, kThreads, 0, st>>>(gen_cfg_of<double>(cfg), index0, n, o, stats_dev,
+                                                                          sc.part, InP<double>{}, SvdBuf<double>{});
   if ((rc = launched("k_study")) != KOG_OK) return rc;
   k_study_finish<<<1, kThreads, 0, st>>>(stats_dev, sc.part, grid);
   return launched("k_study_finish");

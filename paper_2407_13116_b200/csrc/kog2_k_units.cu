@@ -239,7 +239,7 @@ int launch_generate(const kog_run_config* cfg, uint64_t index0, const MatC* out,
   if (!cfg || !mat_ok<T>(out)) return kog2_arg_error("kog_generate_batch: null argument");
   if (kog_validate(cfg) != KOG_OK) return KOG_ERR_ARG;
   if (n == 0) return KOG_OK;
-  k_generate<T><<<grid_for(n), kThreads, 0, st>>>(gen_cfg_of(cfg), index0, out->g11, out->g12, out->g21,
+  k_generate<T><<<grid_for(n), kThreads, 0, st>>>(gen_cfg_of<T>(cfg), index0, out->g11, out->g12, out->g21,
                                                    out->g22, n);
   return launched("k_generate");
 }
