@@ -72,7 +72,8 @@ src_lines = {}
 fp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2407_13116_b200", "csrc", focus)
 if os.path.exists(fp):
     src_lines = {i + 1: l.strip() for i, l in enumerate(open(fp))}
-for s, c in sorted(agg.items(), key=lambda kv: -kv[1]["n"])[:top]:
+key = os.environ.get("SORT", "n")  # n | mov | fp64
+for s, c in sorted(agg.items(), key=lambda kv: -kv[1][key])[:top]:
     ln = int(s.split(":")[1]) if s.startswith(focus) else 0
     print(f"{c['n'] / count * 32:7.1f} {c['n'] / tot * 100:5.1f}%  mov {c['mov'] / max(c['n'], 1) * 100:3.0f}%  fp64 "
           f"{c['fp64'] / max(c['n'], 1) * 100:3.0f}%  lanes {c['t'] / max(c['n'], 1):4.1f}  {s:22s} {src_lines.get(ln, '')[:70]}")
