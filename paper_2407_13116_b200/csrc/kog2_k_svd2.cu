@@ -2,7 +2,7 @@
 // structure-of-arrays device buffers, one thread per matrix, compact result
 // layout of include/kog2.h.
 //
-// binary64 with the default Options runs in two stream-ordered launches:
+// The default Options run in two stream-ordered launches:
 //   k_svd2_fast  the specialised straight-line path (kog2_fast.cuh) over the
 //                whole batch; every lane writes its result, and lanes whose
 //                input leaves that path's domain append their index to a
@@ -10,7 +10,9 @@
 //   k_svd2_list  the general algorithm (kog2_svd2.cuh) over the listed
 //                indices only, overwriting those results — full warps of
 //                deferred work instead of divergent lanes in every warp.
-// Other Options and binary32 run the general kernel over the batch.
+// binary32 with the default Options takes the same two launches (the
+// binary32 instantiation of kog2_fast.cuh); other Options run the general
+// kernel over the batch.
 #include <cstdlib>
 
 #include "kog2_common.cuh"
@@ -69,12 +71,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_svd2(InP<T> in, OutP<T> out, ui
 #ifndef KOG2_FAST_MINB
 #define KOG2_FAST_MINB 4
 #endif
+template <class T>
 __global__ void __launch_bounds__(kThreads, KOG2_FAST_MINB)
-    k_svd2_fast(InP<double> in, OutP<double> out, uint64_t n, uint32_t* list, unsigned* count) {
+    k_svd2_fast(InP<T> in, OutP<T> out, uint64_t n, uint32_t* list, unsigned* count) {
   const unsigned lane = threadIdx.x & 31u;
   for (uint64_t i = gtid(); i < n; i += gstride()) {
-    const Mat<double> g{ld_cs(in.g11 + i), ld_cs(in.g12 + i), ld_cs(in.g21 + i), ld_cs(in.g22 + i)};
-    Result<double> r;
+    const Mat<T> g{ld_cs(in.g11 + i), ld_cs(in.g12 + i), ld_cs(in.g21 + i), ld_cs(in.g22 + i)};
+    Result<T> r;
     bool bad = false;
     fast::svd2_fast(g, r, bad);
     store_result(out, i, r);
@@ -91,14 +94,15 @@ __global__ void __launch_bounds__(kThreads, KOG2_FAST_MINB)
 }
 
 // the general algorithm over the deferred indices (gathered loads/stores)
+template <class T>
 __global__ void __launch_bounds__(kThreads, 3)
-    k_svd2_list(InP<double> in, OutP<double> out, const uint32_t* list, const unsigned* count) {
+    k_svd2_list(InP<T> in, OutP<T> out, const uint32_t* list, const unsigned* count) {
   const uint64_t cnt = *count;
   for (uint64_t k = gtid(); k < cnt; k += gstride()) {
     const uint64_t i = list[k];
-    const Mat<double> g{in.g11[i], in.g12[i], in.g21[i], in.g22[i]};
-    Result<double> r;
-    svd2<double>(g, opt_default(), r);
+    const Mat<T> g{in.g11[i], in.g12[i], in.g21[i], in.g22[i]};
+    Result<T> r;
+    svd2<T>(g, opt_default(), r);
     store_result(out, i, r);
   }
 }
@@ -143,7 +147,7 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
     return kog2_arg_error("kog_svd2_batch: null array pointer");
   const Opt o = opt_of(opt);
   static const bool general_only = std::getenv("KOG2_SVD2_GENERAL") != nullptr;  // A/B comparisons
-  if constexpr (sizeof(T) == 8) {
+  {
     if (opt_is_default(o) && !general_only) {
       Scratch* sc = nullptr;
       int rc = scratch_for(n < kFastChunk ? n : kFastChunk, sc);
@@ -155,9 +159,9 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
                          op.u12 + lo,    op.v11 + lo,    op.v12 + lo,    op.s + lo,      op.flags + lo};
         if (cudaMemsetAsync(sc->count, 0, sizeof(unsigned), st) != cudaSuccess)
           return kog2_cuda_error("cudaMemsetAsync(defer count)");
-        k_svd2_fast<<<grid_for(len), kThreads, 0, st>>>(ip, ol, len, sc->list, sc->count);
+        k_svd2_fast<T><<<grid_for(len), kThreads, 0, st>>>(ip, ol, len, sc->list, sc->count);
         if ((rc = launched("k_svd2_fast")) != KOG_OK) return rc;
-        k_svd2_list<<<148 * 6, kThreads, 0, st>>>(ip, ol, sc->list, sc->count);
+        k_svd2_list<T><<<148 * 6, kThreads, 0, st>>>(ip, ol, sc->list, sc->count);
         if ((rc = launched("k_svd2_list")) != KOG_OK) return rc;
       }
       return KOG_OK;

@@ -19,7 +19,7 @@ lib = capi.load()
 fn = lib.kog2_fast_stats
 fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 buf = (C.c_ulonglong * 96)()
-for k in (1, 2, 3):
+for k in (1, 2, 3, 4):
     c = configs.cfg(k, count=1 << 22)
     g = K.generate(c, 0, c.count)
     torch.cuda.synchronize()
