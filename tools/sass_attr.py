@@ -16,7 +16,8 @@ import tempfile
 rep, kern, obj, count = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
 focus = sys.argv[5] if len(sys.argv) > 5 else "kog2_fast.cuh"
 top = int(sys.argv[6]) if len(sys.argv) > 6 else 40
-depth = int(os.environ.get("DEPTH", "1"))  # 2: attribute to the caller of the innermost focus frame
+depth = int(os.environ.get("DEPTH", "1"))
+# DISASM_KERNEL: regex on the mangled name when KERNEL_REGEX (demangled, for ncu) matches several cubin functions  # 2: attribute to the caller of the innermost focus frame
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
                       "--kernel-name", "regex:" + kern], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
@@ -31,7 +32,7 @@ dis = subprocess.run(["nvdisasm", "-gi", os.path.join(d, cub)], capture_output=T
 kname = None
 for ln in dis:
     m = re.match(r"^(\S+):$", ln)
-    if m and re.search(kern, m.group(1)) and not ln.startswith("."):
+    if m and re.search(os.environ.get("DISASM_KERNEL", kern), m.group(1)) and not ln.startswith("."):
         kname = m.group(1)
         break
 start = dis.index(kname + ":")
