@@ -77,6 +77,11 @@ def _dist(name: str, seed: int, dt=np.float64) -> np.ndarray:
         for row, bit in ((0, 1), (2, 2), (1, 4), (3, 8)):
             v[row] = np.where((t & bit) != 0, v[row], 0.0)
         return v
+    if name == "moderate":  # entry ratios within 2^+-90: tan(2phi) and tan(psi) sweep the closed-form
+        # thresholds of the fast path (2^-27 and 2^54) continuously
+        g = np.stack([_gen.stratified(dt, seed, N, -45, 45, k) for k in range(4)])
+        g[2] = np.where(rng.integers(0, 2, N) == 0, 0.0, g[2])  # half upper-triangular (t ~ 13)
+        return g
     if name == "subnormal_mix":  # subnormal entries next to normal ones (deferred lanes)
         g = np.stack([_gen.any_finite(dt, seed, N, k) for k in range(4)])
         return g
@@ -84,7 +89,7 @@ def _dist(name: str, seed: int, dt=np.float64) -> np.ndarray:
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
-@pytest.mark.parametrize("name", ["wide", "narrow", "near_ties", "rank", "mono_simple", "subnormal_mix"])
+@pytest.mark.parametrize("name", ["wide", "narrow", "near_ties", "rank", "mono_simple", "moderate", "subnormal_mix"])
 def test_fast_path_stress(cuda, ref, name, dt):
     g = np.ascontiguousarray(_dist(name, 0x5EED0000 + zlib.crc32(name.encode()) % 1000, dt))
     assert np.isfinite(g).all()
