@@ -41,8 +41,8 @@ __device__ __forceinline__ uint32_t sign_flags(const Result<T>& r) {
   return f;
 }
 
-template <class T>
-__device__ __forceinline__ void store_result(const OutP<T>& out, uint64_t i, const Result<T>& r) {
+template <class T, class I>
+__device__ __forceinline__ void store_result(const OutP<T>& out, I i, const Result<T>& r) {
   st_cs(out.sig1_f + i, r.sigma1.f);
   st_cs(out.sig2_f + i, r.sigma2.f);
   st_cs(out.sig1_e + i, static_cast<int32_t>(r.sigma1.e));
@@ -75,7 +75,10 @@ template <class T>
 __global__ void __launch_bounds__(kThreads, KOG2_FAST_MINB)
     k_svd2_fast(InP<T> in, OutP<T> out, uint64_t n, uint32_t* list, unsigned* count) {
   const unsigned lane = threadIdx.x & 31u;
-  for (uint64_t i = gtid(); i < n; i += gstride()) {
+  // 32-bit indices: n <= kFastChunk = 2^31 per launch, so i + stride < 2^32
+  // (one 32x32->64 multiply-add per array address instead of 64-bit arithmetic)
+  const unsigned n32 = static_cast<unsigned>(n), stride = gridDim.x * blockDim.x;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n32; i += stride) {
     const Mat<T> g{ld_cs(in.g11 + i), ld_cs(in.g12 + i), ld_cs(in.g21 + i), ld_cs(in.g22 + i)};
     Result<T> r;
     bool bad = false;
@@ -88,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, KOG2_FAST_MINB)
       unsigned base = 0;
       if (static_cast<int>(lane) == leader) base = atomicAdd(count, static_cast<unsigned>(__popc(m)));
       base = __shfl_sync(active, base, leader);
-      if (bad) list[base + __popc(m & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+      if (bad) list[base + __popc(m & ((1u << lane) - 1u))] = i;
     }
   }
 }
