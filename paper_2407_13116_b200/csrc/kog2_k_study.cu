@@ -167,7 +167,7 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 
 template <class T, int ROUTINE, bool PHASED>
 #ifndef KOG2_STUDY_MINB
-#define KOG2_STUDY_MINB 4  // measured (phased, cfg5 rule): 2 -> 950, 3 -> 980, 4 -> 1010 M matrices/s
+#define KOG2_STUDY_MINB 2  // measured with the inline Xf metrics (phased, cfg5 rule, M matrices/s): 2 -> 1416, 3 -> 863, 4 -> 1263
 #endif
 __global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB)
     k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt, kog_stats* stats, BlockPartial* partial, InP<T> gin,
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB)
       mV = fmax(mV, m.reV);
       if (m.kappa_inf) {
         kinf = true;
-      } else if (ext_cmp(m.kappa2, kb.k) > 0) {  // kb.k starts at zero like maxKappa2
+      } else if (xf_cmp(xf_of(m.kappa2), xf_of(kb.k)) > 0) {  // kb.k starts at zero like maxKappa2
         kb.k = m.kappa2;  // a lane's indices increase: first occurrence kept
         kb.idx = index;
         kb.valid = true;

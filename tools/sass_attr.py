@@ -18,6 +18,7 @@ focus = sys.argv[5] if len(sys.argv) > 5 else "kog2_fast.cuh"
 top = int(sys.argv[6]) if len(sys.argv) > 6 else 40
 depth = int(os.environ.get("DEPTH", "1"))
 # DISASM_KERNEL: regex on the mangled name when KERNEL_REGEX (demangled, for ncu) matches several cubin functions  # 2: attribute to the caller of the innermost focus frame
+# FUNCS=1: attribute to the enclosing function (kernel or noinline callee) instead of a source line
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
                       "--kernel-name", "regex:" + kern], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
@@ -27,21 +28,28 @@ ex = [(int(r[0], 16), float(r[ii] or 0), float(r[it] or 0), r[isrc].strip()) for
 base = ex[0][0]
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, capture_output=True)
-cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
-dis = subprocess.run(["nvdisasm", "-gi", os.path.join(d, cub)], capture_output=True, text=True).stdout.splitlines()
 kname = None
-for ln in dis:
-    m = re.match(r"^(\S+):$", ln)
-    if m and re.search(os.environ.get("DISASM_KERNEL", kern), m.group(1)) and not ln.startswith("."):
-        kname = m.group(1)
+for cub in sorted(f for f in os.listdir(d) if f.endswith(".cubin")):  # the cubin that holds the kernel
+    dis = subprocess.run(["nvdisasm", "-gi", os.path.join(d, cub)], capture_output=True, text=True).stdout.splitlines()
+    for ln in dis:
+        m = re.match(r"^(\S+):$", ln)
+        if m and re.search(os.environ.get("DISASM_KERNEL", kern), m.group(1)) and not ln.startswith("."):
+            kname = m.group(1)
+            break
+    if kname:
         break
 start = dis.index(kname + ":")
+func = kname
 site = {}
 chain = []
 last_addr_line = False
 for ln in dis[start + 1:]:
-    if ln.startswith(".text.") or (re.match(r"^\S+:$", ln) and not ln.startswith(".L")):
+    if ln.startswith(".text."):  # the kernel's section ends (it holds its noinline callees too)
         break
+    m = re.match(r"^(\S+):$", ln)
+    if m and not ln.startswith(".L"):  # a callee's entry label
+        func = m.group(1)
+        continue
     m = re.match(r"\s*//## File \"([^\"]+)\", line (\d+)(?: inlined at \"([^\"]+)\", line (\d+))?", ln)
     if m:
         if last_addr_line:
@@ -54,7 +62,7 @@ for ln in dis[start + 1:]:
         last_addr_line = True
         fr = [f"{f}:{l}" for f, l in chain if f == focus]
         s = fr[min(depth, len(fr)) - 1] if fr else (chain[-1][0] + ":" + str(chain[-1][1]) if chain else "?")
-        site[int(m.group(1), 16)] = s
+        site[int(m.group(1), 16)] = ("fn " + func.split("$")[-1][-60:]) if os.environ.get("FUNCS") else s
 agg = collections.defaultdict(lambda: collections.Counter())
 tot = 0.0
 for a, n, t, src in ex:
