@@ -3,6 +3,8 @@
 // and the fused study kernel generate -> svd2_ext -> svd2 | lasv2 ->
 // finiteness -> metrics -> ErrorStats absorb (harness.hpp:190-222), reduced
 // with warp shuffles, shared memory and order-independent global atomics.
+#include <cstdlib>
+
 #include "kog2_common.cuh"
 #include "kog2_ext.cuh"
 #include "kog2_gen.cuh"
@@ -171,7 +173,7 @@ template <class T, int ROUTINE, bool PHASED>
 #endif
 __global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB)
     k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt, kog_stats* stats, BlockPartial* partial, InP<T> gin,
-            SvdBuf<T> sb) {
+            SvdBuf<T> sb, bool accumulate) {
   __shared__ unsigned cnt[19];
   __shared__ double red[5][kThreads / 32];
   __shared__ Ext kred_k[kThreads / 32];
@@ -301,6 +303,10 @@ __global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB)
     atomic_max_nonneg(&stats->reU, v[3]);
     atomic_max_nonneg(&stats->reV, v[4]);
     KappaBest best{ext_zero(), 0ull, false};
+    if (accumulate) {  // this block's slot from the earlier chunks of the study (the merge is order-free)
+      const BlockPartial old = partial[blockIdx.x];
+      if (old.valid) best = KappaBest{Ext{old.k.e, old.k.hi, old.k.lo}, old.idx, true};
+    }
     for (int w = 0; w < kThreads / 32; ++w)
       if (kred_v[w] && kappa_better(kred_k[w], kred_i[w], best.k, best.idx, best.valid)) {
         best.k = kred_k[w];
@@ -390,10 +396,23 @@ struct StudyScratch {
 };
 thread_local StudyScratch g_study[64];
 
-int study_grid(uint64_t n, int sms) {
+#ifndef KOG2_STUDY_BPS_DEFAULT
+#define KOG2_STUDY_BPS_DEFAULT 8
+#endif
+// grid of the study kernels: at most `per_sm` blocks per SM (grid-stride loops)
+int study_grid(uint64_t n, int sms, int per_sm = 8) {
   uint64_t want = (n + kThreads - 1) / kThreads;
-  const uint64_t cap = static_cast<uint64_t>(sms) * 8ull;
+  const uint64_t cap = static_cast<uint64_t>(sms) * static_cast<uint64_t>(per_sm);
   return static_cast<int>(want > cap ? cap : want);
+}
+// the phased k_study's blocks per SM (KOG2_STUDY_BPS overrides, for tuning)
+int study_bps() {
+  static const int v = [] {
+    const char* e = std::getenv("KOG2_STUDY_BPS");
+    const int x = e ? std::atoi(e) : 0;
+    return x > 0 ? x : KOG2_STUDY_BPS_DEFAULT;
+  }();
+  return v;
 }
 
 int study_partials(StudyScratch& sc, int grid) {
@@ -459,22 +478,26 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
   const InP<T> gin{t, t + C, t + 2 * C, t + 3 * C};
   const SvdBuf<T> sb{om.sig1_f, om.sig2_f, om.sig1_e, om.sig2_e, om.u11, om.u12, om.v11,
                      om.v12,    om.flags,  rq,        rq + C,    rd + 2 * C, rd + 3 * C, rd + 4 * C, rd + 5 * C};
-  int rc = study_partials(sc, study_grid(C, sms));
+  const int gmax = study_grid(C, sms, study_bps());
+  int rc = study_partials(sc, gmax);
   if (rc != KOG_OK) return rc;
+  // every slot starts empty; each chunk's blocks merge into their own slot and
+  // k_study_finish merges the slots once at the end
+  if (cudaMemsetAsync(sc.part, 0, sizeof(BlockPartial) * gmax, st) != cudaSuccess)
+    return kog2_cuda_error("cudaMemsetAsync(study partials)");
   for (uint64_t lo = 0; lo < n; lo += C) {
     const uint64_t len = n - lo < C ? n - lo : C;
     if ((rc = Abi<T>::gen(cfg, index0 + lo, &gm, len, st)) != KOG_OK) return rc;
     if ((rc = Abi<T>::svd(&gm, &om, len, &cfg->options, st)) != KOG_OK) return rc;
     k_ref_sigma<T><<<grid_for(len), kThreads, 0, st>>>(gin, sb, len);
     if ((rc = launched("k_ref_sigma")) != KOG_OK) return rc;
-    const int grid = study_grid(len, sms);
+    const int grid = study_grid(len, sms, study_bps());
     k_study<T, KOG_ROUTINE_KOG, true><<<grid, kThreads, 0, st>>>(GenCfg{}, index0 + lo, len, Opt{}, stats, sc.part,
-                                                                  gin, sb);
+                                                                  gin, sb, true);
     if ((rc = launched("k_study")) != KOG_OK) return rc;
-    k_study_finish<<<1, kThreads, 0, st>>>(stats, sc.part, grid);
-    if ((rc = launched("k_study_finish")) != KOG_OK) return rc;
   }
-  return KOG_OK;
+  k_study_finish<<<1, kThreads, 0, st>>>(stats, sc.part, gmax);
+  return launched("k_study_finish");
 }
 
 }  // namespace
@@ -532,10 +555,10 @@ int kog_study_batch(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_
   const Opt o = opt_of(&cfg->options);
   if (cfg->single_precision)
     k_study<float, KOG_ROUTINE_LASV2, false><<<grid, kThreads, 0, st>>>(gen_cfg_of<float>(cfg), index0, n, o, stats_dev,
-                                                                         sc.part, InP<float>{}, SvdBuf<float>{});
+                                                                         sc.part, InP<float>{}, SvdBuf<float>{}, false);
   else
     k_study<double, KOG_ROUTINE_LASV2, false><<<grid, kThreads, 0, st>>>(gen_cfg_of<double>(cfg), index0, n, o, stats_dev,
-                                                                          sc.part, InP<double>{}, SvdBuf<double>{});
+                                                                          sc.part, InP<double>{}, SvdBuf<double>{}, false);
   if ((rc = launched("k_study")) != KOG_OK) return rc;
   k_study_finish<<<1, kThreads, 0, st>>>(stats_dev, sc.part, grid);
   return launched("k_study_finish");
