@@ -71,8 +71,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_svd2(InP<T> in, OutP<T> out, ui
 #ifndef KOG2_FAST_MINB
 #define KOG2_FAST_MINB 4
 #endif
+#ifndef KOG2_FAST_THREADS
+#define KOG2_FAST_THREADS 256
+#endif
 template <class T>
-__global__ void __launch_bounds__(kThreads, KOG2_FAST_MINB)
+__global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
     k_svd2_fast(InP<T> in, OutP<T> out, uint64_t n, uint32_t* list, unsigned* count) {
   const unsigned lane = threadIdx.x & 31u;
   // 32-bit indices: n <= kFastChunk = 2^31 per launch, so i + stride < 2^32
@@ -162,7 +165,7 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
                          op.u12 + lo,    op.v11 + lo,    op.v12 + lo,    op.s + lo,      op.flags + lo};
         if (cudaMemsetAsync(sc->count, 0, sizeof(unsigned), st) != cudaSuccess)
           return kog2_cuda_error("cudaMemsetAsync(defer count)");
-        k_svd2_fast<T><<<grid_for(len), kThreads, 0, st>>>(ip, ol, len, sc->list, sc->count);
+        k_svd2_fast<T><<<grid_for(len, KOG2_FAST_THREADS), KOG2_FAST_THREADS, 0, st>>>(ip, ol, len, sc->list, sc->count);
         if ((rc = launched("k_svd2_fast")) != KOG_OK) return rc;
         k_svd2_list<T><<<148 * 6, kThreads, 0, st>>>(ip, ol, sc->list, sc->count);
         if ((rc = launched("k_svd2_list")) != KOG_OK) return rc;

@@ -434,6 +434,25 @@ def test_svd2_ext_and_metrics(cuda, ref, dt):
     assert bad.size == 0, f"{bad.size} metric records differ; first {bad[0]}: {g[:, bad[0]]}"
 
 
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_metrics_records_on_configs(cuda, ref, k):
+    """Per-matrix error measures (svd2 -> svd2_ext -> metrics, the inline Xf
+    arithmetic on finite data) bit-exact against the reference's metrics() on
+    each BASELINE config's generated matrices (the study's own inputs)."""
+    n = 1 << 15
+    cfg = configs.cfg(k, count=n)
+    off = 0 if k < 5 else (1 << 28) + 12345  # config 5: an index window past config 3's range
+    g = refbind.generate(ref, cfg.c(), off, n)
+    gm = K.metrics(dev(g))
+    wm = refbind.records(capi.kog_metrics, n)
+    (ref.metrics_f64 if g.dtype == np.float64 else ref.metrics_f32)(C.byref(refbind.mat(g)), C.addressof(wm), n,
+                                                                    C.byref(capi.default_options()), 0)
+    gb = np.frombuffer(bytes(gm), dtype=np.uint8).reshape(n, -1)
+    wb = np.frombuffer(bytes(wm), dtype=np.uint8).reshape(n, -1)
+    bad = np.nonzero((gb != wb).any(axis=1))[0]
+    assert bad.size == 0, f"config {k}: {bad.size} metric records differ; first {bad[0]}: {g[:, bad[0]]}"
+
+
 # ----------------------------------------------------------- harness
 APPENDIX_B = [  # SURVEY.md Appendix B: reference CSV rows captured in the survey container
     "double,gen,circ,0,1048576,0000000000c0ffee,kog,5.262556799095865e-16,4.469753940626907e-16,5.475477442600766e-16,4.740088882553483e-16,4.726642799363624e-16,14512464.951216837",
