@@ -167,18 +167,22 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
 }
 
-template <class T, int ROUTINE, bool PHASED>
 #ifndef KOG2_STUDY_MINB
 #define KOG2_STUDY_MINB 2  // measured with the inline Xf metrics (phased, cfg5 rule, M matrices/s): 2 -> 1416, 3 -> 863, 4 -> 1263
 #endif
-__global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB)
+#ifndef KOG2_STUDY_THREADS
+#define KOG2_STUDY_THREADS 256
+#endif
+constexpr int kStudyThreads = KOG2_STUDY_THREADS;
+template <class T, int ROUTINE, bool PHASED>
+__global__ void __launch_bounds__(kStudyThreads, KOG2_STUDY_MINB)
     k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt, kog_stats* stats, BlockPartial* partial, InP<T> gin,
             SvdBuf<T> sb, bool accumulate) {
   __shared__ unsigned cnt[19];
-  __shared__ double red[5][kThreads / 32];
-  __shared__ Ext kred_k[kThreads / 32];
-  __shared__ unsigned long long kred_i[kThreads / 32];
-  __shared__ int kred_v[kThreads / 32];
+  __shared__ double red[5][kStudyThreads / 32];
+  __shared__ Ext kred_k[kStudyThreads / 32];
+  __shared__ unsigned long long kred_i[kStudyThreads / 32];
+  __shared__ int kred_v[kStudyThreads / 32];
   if (threadIdx.x < 19) cnt[threadIdx.x] = 0;
   __syncthreads();
 
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB)
     double v[5];
     for (int k = 0; k < 5; ++k) {
       v[k] = 0.0;
-      for (int w = 0; w < kThreads / 32; ++w) v[k] = fmax(v[k], red[k][w]);
+      for (int w = 0; w < kStudyThreads / 32; ++w) v[k] = fmax(v[k], red[k][w]);
     }
     atomic_max_nonneg(&stats->reG, v[0]);
     atomic_max_nonneg(&stats->reS1, v[1]);
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, KOG2_STUDY_MINB)
       const BlockPartial old = partial[blockIdx.x];
       if (old.valid) best = KappaBest{Ext{old.k.e, old.k.hi, old.k.lo}, old.idx, true};
     }
-    for (int w = 0; w < kThreads / 32; ++w)
+    for (int w = 0; w < kStudyThreads / 32; ++w)
       if (kred_v[w] && kappa_better(kred_k[w], kred_i[w], best.k, best.idx, best.valid)) {
         best.k = kred_k[w];
         best.idx = kred_i[w];
@@ -401,7 +405,7 @@ thread_local StudyScratch g_study[64];
 #endif
 // grid of the study kernels: at most `per_sm` blocks per SM (grid-stride loops)
 int study_grid(uint64_t n, int sms, int per_sm = 8) {
-  uint64_t want = (n + kThreads - 1) / kThreads;
+  uint64_t want = (n + kStudyThreads - 1) / kStudyThreads;
   const uint64_t cap = static_cast<uint64_t>(sms) * static_cast<uint64_t>(per_sm);
   return static_cast<int>(want > cap ? cap : want);
 }
@@ -492,7 +496,7 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
     k_ref_sigma<T><<<grid_for(len), kThreads, 0, st>>>(gin, sb, len);
     if ((rc = launched("k_ref_sigma")) != KOG_OK) return rc;
     const int grid = study_grid(len, sms, study_bps());
-    k_study<T, KOG_ROUTINE_KOG, true><<<grid, kThreads, 0, st>>>(GenCfg{}, index0 + lo, len, Opt{}, stats, sc.part,
+    k_study<T, KOG_ROUTINE_KOG, true><<<grid, kStudyThreads, 0, st>>>(GenCfg{}, index0 + lo, len, Opt{}, stats, sc.part,
                                                                   gin, sb, true);
     if ((rc = launched("k_study")) != KOG_OK) return rc;
   }
@@ -554,10 +558,10 @@ int kog_study_batch(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_
   if (rc != KOG_OK) return rc;
   const Opt o = opt_of(&cfg->options);
   if (cfg->single_precision)
-    k_study<float, KOG_ROUTINE_LASV2, false><<<grid, kThreads, 0, st>>>(gen_cfg_of<float>(cfg), index0, n, o, stats_dev,
+    k_study<float, KOG_ROUTINE_LASV2, false><<<grid, kStudyThreads, 0, st>>>(gen_cfg_of<float>(cfg), index0, n, o, stats_dev,
                                                                          sc.part, InP<float>{}, SvdBuf<float>{}, false);
   else
-    k_study<double, KOG_ROUTINE_LASV2, false><<<grid, kThreads, 0, st>>>(gen_cfg_of<double>(cfg), index0, n, o, stats_dev,
+    k_study<double, KOG_ROUTINE_LASV2, false><<<grid, kStudyThreads, 0, st>>>(gen_cfg_of<double>(cfg), index0, n, o, stats_dev,
                                                                           sc.part, InP<double>{}, SvdBuf<double>{}, false);
   if ((rc = launched("k_study")) != KOG_OK) return rc;
   k_study_finish<<<1, kThreads, 0, st>>>(stats_dev, sc.part, grid);
