@@ -219,6 +219,10 @@ def l2_note(nbytes: int) -> str:
             "correctness case, not a bandwidth measurement" % (nbytes / 2**20))
 
 
+SHAPE_OF = {1: "general (circ)", 2: "upper-triangular (e in [-1000,1000])", 3: "general",
+            4: "general (e in [-60,60], 1% subnormal-adjacent)"}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -371,7 +375,7 @@ def main() -> None:
             "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": suf,
             "data": "synthetic (seeded on-device counter-based generator, SURVEY.md §8d)",
-            "config": {"workload": f"cfg{args.config}: {n} general {suf} 2x2 matrices per GPU"
+            "config": {"workload": f"cfg{args.config}: {n} {SHAPE_OF[args.config]} {suf} 2x2 matrices per GPU"
                                    + (f" (e in [-500,500], 1/8 zero patterns); rank r owns indices [r*{n},(r+1)*{n}) of config 5" if args.config == 3 else ""),
                        "model": "enhanced 2x2 Kogbetliantz svd2 (arXiv 2407.13116)", "global_batch": world * n,
                        "parallelism": f"dp{world} (index-range shards, no data-path collective)",
