@@ -397,6 +397,12 @@ struct StudyScratch {
   int blocks = 0;
   void* buf = nullptr;
   size_t cap = 0;
+  // phased study pipeline: a producer stream (generate + svd2, whose deferral
+  // scratch is single-user) and two consumer streams (reference sigma +
+  // metrics) over two chunk buffers; events chain them
+  cudaStream_t prod = nullptr, cons[2] = {nullptr, nullptr};
+  cudaEvent_t ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr}, join[3] = {nullptr, nullptr, nullptr},
+              fork = nullptr;
 };
 thread_local StudyScratch g_study[64];
 
@@ -417,6 +423,19 @@ int study_bps() {
     return x > 0 ? x : KOG2_STUDY_BPS_DEFAULT;
   }();
   return v;
+}
+
+int study_streams(StudyScratch& sc) {
+  if (sc.prod) return KOG_OK;
+  bool ok = cudaStreamCreateWithFlags(&sc.prod, cudaStreamNonBlocking) == cudaSuccess;
+  for (int k = 0; k < 2; ++k) {
+    ok = ok && cudaStreamCreateWithFlags(&sc.cons[k], cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&sc.ready[k], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&sc.freed[k], cudaEventDisableTiming) == cudaSuccess;
+  }
+  for (int k = 0; k < 3; ++k) ok = ok && cudaEventCreateWithFlags(&sc.join[k], cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaEventCreateWithFlags(&sc.fork, cudaEventDisableTiming) == cudaSuccess;
+  return ok ? KOG_OK : kog2_cuda_error("study streams/events");
 }
 
 int study_partials(StudyScratch& sc, int grid) {
@@ -464,7 +483,9 @@ template <class T>
 int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats, StudyScratch& sc, int sms,
                  cudaStream_t st) {
   const uint64_t C = n < kStudyChunk ? n : kStudyChunk;
-  const size_t need = static_cast<size_t>(C) * (6 * 8 + 10 * sizeof(T) + 4 * sizeof(int32_t));
+  const int nbuf = n > C ? 2 : 1;  // two chunk buffers when there is more than one chunk
+  const size_t per = static_cast<size_t>(C) * (6 * 8 + 10 * sizeof(T) + 4 * sizeof(int32_t));
+  const size_t need = per * nbuf;
   if (sc.cap < need) {
     if (sc.buf) cudaFree(sc.buf);
     sc.buf = nullptr;
@@ -472,35 +493,66 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
     if (cudaMalloc(&sc.buf, need) != cudaSuccess) return kog2_cuda_error("cudaMalloc(study chunk)");
     sc.cap = need;
   }
-  double* rd = static_cast<double*>(sc.buf);  // the 8-byte reference arrays first (alignment)
-  long long* rq = reinterpret_cast<long long*>(rd);
-  T* t = reinterpret_cast<T*>(rd + 6 * C);
-  int32_t* w = reinterpret_cast<int32_t*>(t + 10 * C);
-  const typename Abi<T>::Mat gm{t, t + C, t + 2 * C, t + 3 * C};
-  const typename Abi<T>::Out om{t + 4 * C, t + 5 * C, w,         w + C,     t + 6 * C,
-                                t + 7 * C, t + 8 * C, t + 9 * C, w + 2 * C, reinterpret_cast<uint32_t*>(w + 3 * C)};
-  const InP<T> gin{t, t + C, t + 2 * C, t + 3 * C};
-  const SvdBuf<T> sb{om.sig1_f, om.sig2_f, om.sig1_e, om.sig2_e, om.u11, om.u12, om.v11,
-                     om.v12,    om.flags,  rq,        rq + C,    rd + 2 * C, rd + 3 * C, rd + 4 * C, rd + 5 * C};
-  const int gmax = study_grid(C, sms, study_bps());
-  int rc = study_partials(sc, gmax);
+  int rc = study_streams(sc);
   if (rc != KOG_OK) return rc;
-  // every slot starts empty; each chunk's blocks merge into their own slot and
-  // k_study_finish merges the slots once at the end
-  if (cudaMemsetAsync(sc.part, 0, sizeof(BlockPartial) * gmax, st) != cudaSuccess)
+  struct Bufs {
+    typename Abi<T>::Mat gm;
+    typename Abi<T>::Out om;
+    InP<T> gin;
+    SvdBuf<T> sb;
+  } bufs[2];
+  for (int k = 0; k < nbuf; ++k) {
+    double* rd = reinterpret_cast<double*>(static_cast<char*>(sc.buf) + per * k);  // the 8-byte arrays first
+    long long* rq = reinterpret_cast<long long*>(rd);
+    T* t = reinterpret_cast<T*>(rd + 6 * C);
+    int32_t* w = reinterpret_cast<int32_t*>(t + 10 * C);
+    bufs[k].gm = typename Abi<T>::Mat{t, t + C, t + 2 * C, t + 3 * C};
+    const typename Abi<T>::Out om{t + 4 * C, t + 5 * C, w,         w + C,     t + 6 * C,
+                                  t + 7 * C, t + 8 * C, t + 9 * C, w + 2 * C, reinterpret_cast<uint32_t*>(w + 3 * C)};
+    bufs[k].om = om;
+    bufs[k].gin = InP<T>{t, t + C, t + 2 * C, t + 3 * C};
+    bufs[k].sb = SvdBuf<T>{om.sig1_f, om.sig2_f, om.sig1_e, om.sig2_e, om.u11, om.u12, om.v11,
+                           om.v12,    om.flags,  rq,        rq + C,    rd + 2 * C, rd + 3 * C, rd + 4 * C, rd + 5 * C};
+  }
+  const int gmax = study_grid(C, sms, study_bps());
+  // one set of per-block kappa slots per consumer stream (concurrent k_study
+  // launches never share a slot); every slot starts empty, each chunk's blocks
+  // merge into their own slot, and k_study_finish merges all slots at the end
+  if ((rc = study_partials(sc, 2 * gmax)) != KOG_OK) return rc;
+  if (cudaMemsetAsync(sc.part, 0, sizeof(BlockPartial) * 2 * gmax, st) != cudaSuccess)
     return kog2_cuda_error("cudaMemsetAsync(study partials)");
-  for (uint64_t lo = 0; lo < n; lo += C) {
+  // fork from the caller's stream
+  cudaEventRecord(sc.fork, st);
+  cudaStreamWaitEvent(sc.prod, sc.fork, 0);
+  cudaStreamWaitEvent(sc.cons[0], sc.fork, 0);
+  cudaStreamWaitEvent(sc.cons[1], sc.fork, 0);
+  uint64_t c = 0;
+  for (uint64_t lo = 0; lo < n; lo += C, ++c) {
     const uint64_t len = n - lo < C ? n - lo : C;
-    if ((rc = Abi<T>::gen(cfg, index0 + lo, &gm, len, st)) != KOG_OK) return rc;
-    if ((rc = Abi<T>::svd(&gm, &om, len, &cfg->options, st)) != KOG_OK) return rc;
-    k_ref_sigma<T><<<grid_for(len), kThreads, 0, st>>>(gin, sb, len);
+    const int k = static_cast<int>(c & 1);
+    Bufs& bf = bufs[nbuf == 2 ? k : 0];
+    cudaStream_t q = sc.cons[k];
+    // producer: generate + svd2 into buffer k once its previous consumer is done
+    if (c >= 2) cudaStreamWaitEvent(sc.prod, sc.freed[k], 0);
+    if ((rc = Abi<T>::gen(cfg, index0 + lo, &bf.gm, len, sc.prod)) != KOG_OK) return rc;
+    if ((rc = Abi<T>::svd(&bf.gm, &bf.om, len, &cfg->options, sc.prod)) != KOG_OK) return rc;
+    cudaEventRecord(sc.ready[k], sc.prod);
+    // consumer k: reference sigma + metrics + ErrorStats
+    cudaStreamWaitEvent(q, sc.ready[k], 0);
+    k_ref_sigma<T><<<grid_for(len), kThreads, 0, q>>>(bf.gin, bf.sb, len);
     if ((rc = launched("k_ref_sigma")) != KOG_OK) return rc;
     const int grid = study_grid(len, sms, study_bps());
-    k_study<T, KOG_ROUTINE_KOG, true><<<grid, kStudyThreads, 0, st>>>(GenCfg{}, index0 + lo, len, Opt{}, stats, sc.part,
-                                                                  gin, sb, true);
+    k_study<T, KOG_ROUTINE_KOG, true><<<grid, kStudyThreads, 0, q>>>(GenCfg{}, index0 + lo, len, Opt{}, stats,
+                                                                   sc.part + k * gmax, bf.gin, bf.sb, true);
     if ((rc = launched("k_study")) != KOG_OK) return rc;
+    cudaEventRecord(sc.freed[k], q);
   }
-  k_study_finish<<<1, kThreads, 0, st>>>(stats, sc.part, gmax);
+  // join back into the caller's stream
+  cudaEventRecord(sc.join[0], sc.prod);
+  cudaEventRecord(sc.join[1], sc.cons[0]);
+  cudaEventRecord(sc.join[2], sc.cons[1]);
+  for (int k = 0; k < 3; ++k) cudaStreamWaitEvent(st, sc.join[k], 0);
+  k_study_finish<<<1, kThreads, 0, st>>>(stats, sc.part, 2 * gmax);
   return launched("k_study_finish");
 }
 
