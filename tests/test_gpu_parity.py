@@ -392,6 +392,40 @@ def test_svd2_baseline_configs(cuda, ref, k):
     _gen.assert_bits_equal(host(g2).ravel(), refbind.generate(ref, cfg.c(), off, 4096).ravel(), "offset window")
 
 
+@pytest.mark.parametrize("k,count", [(3, 1 << 28), (4, 1 << 28), (2, 1 << 26)])
+def test_svd2_full_size_sampled(cuda, ref, k, count):
+    """BASELINE configs at their full sizes (the bench workloads): one svd2 call
+    over the whole on-device batch, then bit-exact parity on 64 seeded windows
+    of 4096 matrices (the counter-based generator reproduces any window on the
+    host), plus size-independent properties over every matrix: no domain
+    errors, sigma1 >= sigma2 >= 0 as pairs, and |u11|^2 + |u12|^2 = 1 to
+    working accuracy."""
+    cfg = configs.cfg(k, count=count)
+    g = K.generate(cfg, 0, count)
+    r = K.svd2(g)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0xF0115)
+    W = 4096
+    offs = sorted(rng.integers(0, count - W, 64).tolist()) + [0, count - W]
+    for off in offs:
+        gw = refbind.generate(ref, cfg.c(), off, W)
+        want = refbind.svd2(ref, gw)
+        got = {key: v[off:off + W] for key, v in r.items()}
+        compare_svd(got, want, f"cfg{k} window {off}")
+    assert capi.F_DOMAIN_ERROR == 1 << 31
+    assert int((r["flags"].view(torch.int32) < 0).sum()) == 0  # the domain-error bit is the sign bit
+    e1, e2 = r["sig1_e"].long(), r["sig2_e"].long()
+    f1, f2 = r["sig1_f"].double(), r["sig2_f"].double()
+    assert bool((f2 >= 0).all()) and bool((f1 >= 0).all())
+    z2 = f2 == 0
+    assert bool((z2 | (e1 > e2) | ((e1 == e2) & (f1 >= f2))).all()), "sigma1 < sigma2"
+    u11, u12 = r["u11"].double(), r["u12"].double()
+    eps = 4 * float(np.finfo(np.float32 if k == 4 else np.float64).eps)
+    assert float((u11 * u11 + u12 * u12 - 1).abs().max()) < eps
+    del g, r
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("dt", DTS)
 def test_svd2_host_pipeline(cuda, ref, dt):
     """kog_svd2_host_*: host buffers through the chunked H2D/kernel/D2H pipeline."""
