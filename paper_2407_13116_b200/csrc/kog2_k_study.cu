@@ -522,10 +522,10 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
   if (cudaMemsetAsync(sc.part, 0, sizeof(BlockPartial) * 2 * gmax, st) != cudaSuccess)
     return kog2_cuda_error("cudaMemsetAsync(study partials)");
   // fork from the caller's stream
-  cudaEventRecord(sc.fork, st);
-  cudaStreamWaitEvent(sc.prod, sc.fork, 0);
-  cudaStreamWaitEvent(sc.cons[0], sc.fork, 0);
-  cudaStreamWaitEvent(sc.cons[1], sc.fork, 0);
+  if (cudaEventRecord(sc.fork, st) != cudaSuccess || cudaStreamWaitEvent(sc.prod, sc.fork, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(sc.cons[0], sc.fork, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(sc.cons[1], sc.fork, 0) != cudaSuccess)
+    return kog2_cuda_error("study fork");
   uint64_t c = 0;
   for (uint64_t lo = 0; lo < n; lo += C, ++c) {
     const uint64_t len = n - lo < C ? n - lo : C;
@@ -533,25 +533,25 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
     Bufs& bf = bufs[nbuf == 2 ? k : 0];
     cudaStream_t q = sc.cons[k];
     // producer: generate + svd2 into buffer k once its previous consumer is done
-    if (c >= 2) cudaStreamWaitEvent(sc.prod, sc.freed[k], 0);
+    if (c >= 2 && cudaStreamWaitEvent(sc.prod, sc.freed[k], 0) != cudaSuccess) return kog2_cuda_error("study wait");
     if ((rc = Abi<T>::gen(cfg, index0 + lo, &bf.gm, len, sc.prod)) != KOG_OK) return rc;
     if ((rc = Abi<T>::svd(&bf.gm, &bf.om, len, &cfg->options, sc.prod)) != KOG_OK) return rc;
-    cudaEventRecord(sc.ready[k], sc.prod);
     // consumer k: reference sigma + metrics + ErrorStats
-    cudaStreamWaitEvent(q, sc.ready[k], 0);
+    if (cudaEventRecord(sc.ready[k], sc.prod) != cudaSuccess || cudaStreamWaitEvent(q, sc.ready[k], 0) != cudaSuccess)
+      return kog2_cuda_error("study chunk handoff");
     k_ref_sigma<T><<<grid_for(len), kThreads, 0, q>>>(bf.gin, bf.sb, len);
     if ((rc = launched("k_ref_sigma")) != KOG_OK) return rc;
     const int grid = study_grid(len, sms, study_bps());
     k_study<T, KOG_ROUTINE_KOG, true><<<grid, kStudyThreads, 0, q>>>(GenCfg{}, index0 + lo, len, Opt{}, stats,
                                                                    sc.part + k * gmax, bf.gin, bf.sb, true);
     if ((rc = launched("k_study")) != KOG_OK) return rc;
-    cudaEventRecord(sc.freed[k], q);
+    if (cudaEventRecord(sc.freed[k], q) != cudaSuccess) return kog2_cuda_error("study chunk release");
   }
   // join back into the caller's stream
-  cudaEventRecord(sc.join[0], sc.prod);
-  cudaEventRecord(sc.join[1], sc.cons[0]);
-  cudaEventRecord(sc.join[2], sc.cons[1]);
-  for (int k = 0; k < 3; ++k) cudaStreamWaitEvent(st, sc.join[k], 0);
+  const cudaStream_t sides[3] = {sc.prod, sc.cons[0], sc.cons[1]};
+  for (int k = 0; k < 3; ++k)
+    if (cudaEventRecord(sc.join[k], sides[k]) != cudaSuccess || cudaStreamWaitEvent(st, sc.join[k], 0) != cudaSuccess)
+      return kog2_cuda_error("study join");
   k_study_finish<<<1, kThreads, 0, st>>>(stats, sc.part, 2 * gmax);
   return launched("k_study_finish");
 }
