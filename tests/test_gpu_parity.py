@@ -522,6 +522,8 @@ def test_run_batch_vs_reference_counts(cuda, ref):
                 configs.cfg(3, count=1 << 18), configs.cfg(4, count=1 << 18), configs.cfg(2, count=1 << 18),
                 # more than one 2^22-matrix chunk of the phased study
                 configs.cfg(5, count=(1 << 22) + 4099),
+                # four chunks: both chunk buffers reused by the producer/consumer pipeline, a 5-matrix tail
+                configs.cfg(5, count=3 * (1 << 22) + 5),
                 # non-default Options: the general svd2 kernel inside the study
                 K.RunConfig(shape=capi.SHAPE_GEN, regime=capi.REGIME_BULLET, count=1 << 17, seed=79,
                             options=K.Options(hypot_is_cr=False, ominus_for_d=True)),
