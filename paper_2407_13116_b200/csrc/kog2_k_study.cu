@@ -91,8 +91,12 @@ __device__ __forceinline__ float with_sign(float mag, bool neg) { return neg ? -
 template <class T>
 __device__ __forceinline__ uint32_t run_one_buf(const Mat<T>& g, const SvdBuf<T>& b, uint64_t i, Metrics& m) {
   ExtSvd ref;  // metrics() reads the singular values only
+#ifndef KOG2_STUDY_REF_KERNEL
+  ref_sigma<T>(g, ref);  // computed here (inline Xf) instead of by k_ref_sigma
+#else
   ref.sigma1 = Ext{b.re1[i], b.rh1[i], b.rl1[i]};
   ref.sigma2 = Ext{b.re2[i], b.rh2[i], b.rl2[i]};
+#endif
   uint32_t flags = b.flags[i];
   const T u11 = b.u11[i], u12 = b.u12[i], v11 = b.v11[i], v12 = b.v12[i];
   const Mat<T> u{u11, u12, with_sign(fabs(u12), flags & KOG_F_SIGN_U21), with_sign(fabs(u11), flags & KOG_F_SIGN_U22)};
@@ -539,8 +543,10 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
     // consumer k: reference sigma + metrics + ErrorStats
     if (cudaEventRecord(sc.ready[k], sc.prod) != cudaSuccess || cudaStreamWaitEvent(q, sc.ready[k], 0) != cudaSuccess)
       return kog2_cuda_error("study chunk handoff");
+#ifdef KOG2_STUDY_REF_KERNEL  // (the separate reference-sigma pass, for A/B)
     k_ref_sigma<T><<<grid_for(len), kThreads, 0, q>>>(bf.gin, bf.sb, len);
     if ((rc = launched("k_ref_sigma")) != KOG_OK) return rc;
+#endif
     const int grid = study_grid(len, sms, study_bps());
     k_study<T, KOG_ROUTINE_KOG, true><<<grid, kStudyThreads, 0, q>>>(GenCfg{}, index0 + lo, len, Opt{}, stats,
                                                                    sc.part + k * gmax, bf.gin, bf.sb, true);
