@@ -41,7 +41,7 @@ __global__ void k_svd2_ext(InP<T> in, kog_extsvd* o, uint64_t n) {
 template <class T>
 __device__ __forceinline__ uint32_t run_one_kog(const Mat<T>& g, const Opt& o, Metrics& m) {
   ExtSvd ref;
-  svd2_ext<T, false>(g, ref);  // metrics() reads the singular values only
+  ref_sigma<T>(g, ref);  // metrics() reads the singular values only (inline Xf where it applies)
   Result<T> r;
   svd2<T>(g, o, r);
   uint32_t flags = r.flags;
@@ -111,7 +111,7 @@ __device__ __forceinline__ uint32_t run_one_buf(const Mat<T>& g, const SvdBuf<T>
 template <class T>
 __device__ __forceinline__ uint32_t run_one_lasv2(const Mat<T>& g, Metrics& m) {
   ExtSvd ref;
-  svd2_ext<T, false>(g, ref);  // metrics() reads the singular values only
+  ref_sigma<T>(g, ref);  // metrics() reads the singular values only (inline Xf where it applies)
   const Lasv2<T> r = lasv2(g.g11, g.g12, g.g22);
   const Mat<T> u{r.csl, -r.snl, r.snl, r.csl};
   const Mat<T> v{r.csr, -r.snr, r.snr, r.csr};
