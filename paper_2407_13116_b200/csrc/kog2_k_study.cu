@@ -410,6 +410,9 @@ struct StudyScratch {
 };
 thread_local StudyScratch g_study[64];
 
+#ifndef KOG2_STUDY_STREAMS_DEFAULT
+#define KOG2_STUDY_STREAMS_DEFAULT 1  // two consumer streams ran two k_study at once: erratic 500-1500 M/s at 2^31
+#endif
 #ifndef KOG2_STUDY_BPS_DEFAULT
 #define KOG2_STUDY_BPS_DEFAULT 8
 #endif
@@ -418,6 +421,17 @@ int study_grid(uint64_t n, int sms, int per_sm = 8) {
   uint64_t want = (n + kStudyThreads - 1) / kStudyThreads;
   const uint64_t cap = static_cast<uint64_t>(sms) * static_cast<uint64_t>(per_sm);
   return static_cast<int>(want > cap ? cap : want);
+}
+// streams of the phased study: 0 = everything on the caller's stream, 1 = a
+// producer stream and one consumer stream, 2 = a producer and two consumers
+// (KOG2_STUDY_STREAMS overrides)
+int study_streams_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("KOG2_STUDY_STREAMS");
+    const int x = e ? std::atoi(e) : -1;
+    return x >= 0 && x <= 2 ? x : KOG2_STUDY_STREAMS_DEFAULT;
+  }();
+  return v;
 }
 // the phased k_study's blocks per SM (KOG2_STUDY_BPS overrides, for tuning)
 int study_bps() {
@@ -526,6 +540,9 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
   if (cudaMemsetAsync(sc.part, 0, sizeof(BlockPartial) * 2 * gmax, st) != cudaSuccess)
     return kog2_cuda_error("cudaMemsetAsync(study partials)");
   // fork from the caller's stream
+  const int mode = study_streams_mode();
+  const cudaStream_t prod = mode == 0 ? st : sc.prod;
+  const cudaStream_t cons[2] = {mode == 0 ? st : sc.cons[0], mode == 2 ? sc.cons[1] : (mode == 0 ? st : sc.cons[0])};
   if (cudaEventRecord(sc.fork, st) != cudaSuccess || cudaStreamWaitEvent(sc.prod, sc.fork, 0) != cudaSuccess ||
       cudaStreamWaitEvent(sc.cons[0], sc.fork, 0) != cudaSuccess ||
       cudaStreamWaitEvent(sc.cons[1], sc.fork, 0) != cudaSuccess)
@@ -535,13 +552,13 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
     const uint64_t len = n - lo < C ? n - lo : C;
     const int k = static_cast<int>(c & 1);
     Bufs& bf = bufs[nbuf == 2 ? k : 0];
-    cudaStream_t q = sc.cons[k];
+    cudaStream_t q = cons[k];
     // producer: generate + svd2 into buffer k once its previous consumer is done
-    if (c >= 2 && cudaStreamWaitEvent(sc.prod, sc.freed[k], 0) != cudaSuccess) return kog2_cuda_error("study wait");
-    if ((rc = Abi<T>::gen(cfg, index0 + lo, &bf.gm, len, sc.prod)) != KOG_OK) return rc;
-    if ((rc = Abi<T>::svd(&bf.gm, &bf.om, len, &cfg->options, sc.prod)) != KOG_OK) return rc;
+    if (c >= 2 && cudaStreamWaitEvent(prod, sc.freed[k], 0) != cudaSuccess) return kog2_cuda_error("study wait");
+    if ((rc = Abi<T>::gen(cfg, index0 + lo, &bf.gm, len, prod)) != KOG_OK) return rc;
+    if ((rc = Abi<T>::svd(&bf.gm, &bf.om, len, &cfg->options, prod)) != KOG_OK) return rc;
     // consumer k: reference sigma + metrics + ErrorStats
-    if (cudaEventRecord(sc.ready[k], sc.prod) != cudaSuccess || cudaStreamWaitEvent(q, sc.ready[k], 0) != cudaSuccess)
+    if (cudaEventRecord(sc.ready[k], prod) != cudaSuccess || cudaStreamWaitEvent(q, sc.ready[k], 0) != cudaSuccess)
       return kog2_cuda_error("study chunk handoff");
 #ifdef KOG2_STUDY_REF_KERNEL  // (the separate reference-sigma pass, for A/B)
     k_ref_sigma<T><<<grid_for(len), kThreads, 0, q>>>(bf.gin, bf.sb, len);
