@@ -191,6 +191,38 @@ def cpu_baseline(g_host, single: bool) -> dict:
                       f"std::thread over 4096-blocks, {dt2:.1f} s"}
 
 
+def study_cpu_baseline(K) -> dict | None:
+    """The reference's own run_batch (harness.hpp:226-271, threads=0 = every
+    host thread; oracle/_ref) on a bounded prefix of config 5 (~8 s of wall
+    time), beside the GPU study; the GPU study of the same prefix must print
+    the same CSV row (csv_row, harness.hpp:275-321)."""
+    from oracle import refbind
+    from paper_2407_13116_b200 import configs
+
+    if not refbind.have_ref():
+        return None
+    ref = refbind.ref()
+
+    def run(n):
+        c = configs.cfg(5, count=n)
+        cc = c.c()
+        cc.threads = 0
+        t0 = time.perf_counter()
+        rc, st, msg = refbind.run_batch(ref, cc)
+        dt = time.perf_counter() - t0
+        assert rc == 0, msg
+        return dt, refbind.csv_row(ref, cc, st)
+
+    n = 1 << 20
+    dt, _ = run(n)
+    n = int(min(1 << 27, max(n, (n / dt) * 8.0))) & ~4095
+    dt, row = run(n)
+    gpu = K.csv_row(configs.cfg(5, count=n), K.run_batch(configs.cfg(5, count=n)))
+    return {"value": n / dt, "unit": UNIT, "cores": int(ref.hardware_threads()), "kind": "reference",
+            "sample": f"first {n} config-5 matrices, reference run_batch (oracle/_ref, threads=0), {dt:.1f} s",
+            "csv_equal": gpu == row}
+
+
 def fp64_probe(K, torch) -> dict:
     """Achievable FP64 FMA rate on this GPU (DFMA chains, 8 per thread)."""
     lib = K._lib()
@@ -367,6 +399,8 @@ def main() -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(g_host, base.single_precision)
+        if study is not None:
+            study["cpu_baseline"] = study_cpu_baseline(K)
     fp64 = fp64_probe(K, torch) if rank == 0 else None
 
     if rank == 0:
