@@ -99,6 +99,96 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
   }
 }
 
+#ifdef KOG2_FAST_TMA
+// Experiment (A/B builds only): k_svd2_fast with its input tiles fetched by
+// the bulk-copy engine.  Each warp owns a 32-matrix tile per iteration (the
+// same indices as k_svd2_fast); lane 0 prefetches the warp's tile two
+// iterations ahead into a double-buffered shared-memory slot (four 32-entry
+// cp.async.bulk copies completing on the slot's mbarrier), and the lanes read
+// their entries from shared memory.  The last, partial tile loads directly.
+template <class T>
+struct TmaSlot {
+  T in[2][4][32];
+  unsigned long long mbar[2];
+};
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+template <class T>
+__device__ __forceinline__ void tma_issue(TmaSlot<T>& S, int b, const InP<T>& in, unsigned t) {
+  constexpr unsigned bytes = 32 * sizeof(T);
+  const unsigned mb = smem_u32(&S.mbar[b]);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(4 * bytes) : "memory");
+  const T* src[4] = {in.g11, in.g12, in.g21, in.g22};
+#pragma unroll
+  for (int f = 0; f < 4; ++f)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(&S.in[b][f][0])),
+                 "l"(src[f] + static_cast<size_t>(t) * 32), "r"(bytes), "r"(mb)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned mb, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(mb),
+      "r"(parity)
+      : "memory");
+}
+template <class T>
+__global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
+    k_svd2_fast_tma(InP<T> in, OutP<T> out, uint64_t n, uint32_t* list, unsigned* count) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  TmaSlot<T>& S = reinterpret_cast<TmaSlot<T>*>(smem_raw)[wib];
+  const unsigned n32 = static_cast<unsigned>(n), full = n32 / 32u;
+  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+  const unsigned t0 = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (t0 < full) tma_issue(S, 0, in, t0);
+    if (t0 + nwarps < full) tma_issue(S, 1, in, t0 + nwarps);
+  }
+  __syncwarp();
+  unsigned k = 0;
+  for (unsigned t = t0; t * 32u < n32; t += nwarps, ++k) {
+    const unsigned i = t * 32u + lane;
+    const int b = k & 1;
+    Mat<T> g;
+    if (t < full) {
+      mbar_wait(smem_u32(&S.mbar[b]), (k >> 1) & 1u);
+      g = Mat<T>{S.in[b][0][lane], S.in[b][1][lane], S.in[b][2][lane], S.in[b][3][lane]};
+      __syncwarp();
+      if (lane == 0 && t + 2 * nwarps < full) tma_issue(S, b, in, t + 2 * nwarps);
+    } else {
+      if (i >= n32) break;
+      g = Mat<T>{ld_cs(in.g11 + i), ld_cs(in.g12 + i), ld_cs(in.g21 + i), ld_cs(in.g22 + i)};
+    }
+    Result<T> r;
+    bool bad = false;
+    fast::svd2_fast(g, r, bad);
+    store_result(out, i, r);
+    const unsigned active = __activemask();
+    const unsigned m = __ballot_sync(active, bad);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned base = 0;
+      if (static_cast<int>(lane) == leader) base = atomicAdd(count, static_cast<unsigned>(__popc(m)));
+      base = __shfl_sync(active, base, leader);
+      if (bad) list[base + __popc(m & ((1u << lane) - 1u))] = i;
+    }
+  }
+}
+template <class T>
+bool tma_ok(const InP<T>& ip) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(ip.g11) | reinterpret_cast<uintptr_t>(ip.g12) |
+                      reinterpret_cast<uintptr_t>(ip.g21) | reinterpret_cast<uintptr_t>(ip.g22);
+  return (a & 15u) == 0;
+}
+#endif
+
 // the general algorithm over the deferred indices (gathered loads/stores)
 template <class T>
 __global__ void __launch_bounds__(kThreads, 3)
@@ -165,7 +255,17 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
                          op.u12 + lo,    op.v11 + lo,    op.v12 + lo,    op.s + lo,      op.flags + lo};
         if (cudaMemsetAsync(sc->count, 0, sizeof(unsigned), st) != cudaSuccess)
           return kog2_cuda_error("cudaMemsetAsync(defer count)");
-        k_svd2_fast<T><<<grid_for(len, KOG2_FAST_THREADS), KOG2_FAST_THREADS, 0, st>>>(ip, ol, len, sc->list, sc->count);
+#ifdef KOG2_FAST_TMA
+        if (tma_ok(ip)) {
+          constexpr int smem = (KOG2_FAST_THREADS / 32) * sizeof(TmaSlot<T>);
+          static const bool attr = cudaFuncSetAttribute(k_svd2_fast_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        smem) == cudaSuccess;
+          (void)attr;
+          k_svd2_fast_tma<T><<<grid_for(len, KOG2_FAST_THREADS), KOG2_FAST_THREADS, smem, st>>>(ip, ol, len, sc->list,
+                                                                                               sc->count);
+        } else
+#endif
+          k_svd2_fast<T><<<grid_for(len, KOG2_FAST_THREADS), KOG2_FAST_THREADS, 0, st>>>(ip, ol, len, sc->list, sc->count);
         if ((rc = launched("k_svd2_fast")) != KOG_OK) return rc;
         k_svd2_list<T><<<148 * 6, kThreads, 0, st>>>(ip, ol, sc->list, sc->count);
         if ((rc = launched("k_svd2_list")) != KOG_OK) return rc;
