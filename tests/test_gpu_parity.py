@@ -97,6 +97,37 @@ def test_hypot_exact_ties(cuda, dt):
     _gen.assert_bits_equal(got, ex, "hypot ties")
 
 
+def test_hypotf_near_midpoints(cuda, ref):
+    """binary32 hypot whose exact value lies 2^-58 .. 2^-41.6 (relative) from
+    a rounding midpoint (28% below 2^-46, median 2^-44.8): either side of the
+    fast path's decision tolerance (kog2_fp.cuh hypot_main<float>).  m = M 2^-24 (M odd, 25 bits) is a
+    midpoint, a = (M - 1 - 2t) 2^-24 a float below it, and b the float
+    nearest sqrt(m^2 - a^2) moved by j ulps, so a^2 + b^2 - m^2 is about
+    j 2^-24 of b^2.  Results equal the reference and the exact value."""
+    rng = np.random.default_rng(0x68790005)
+    n = 60_000
+    M = rng.integers(1 << 24, 1 << 25, size=n, dtype=np.int64) | 1
+    t = rng.integers(0, 4, size=n)
+    A = M - 1 - 2 * t
+    c = M * M - A * A
+    b0 = np.sqrt(c.astype(np.float64)) * 2.0 ** -24
+    b = b0.astype(np.float32)
+    j = rng.integers(-3, 4, size=n).astype(np.int32)
+    b = (b.view(np.int32) + j).view(np.float32)
+    x = rng.integers(-40, 41, size=n)
+    a = np.ldexp(A.astype(np.float64) * 2.0 ** -24, x).astype(np.float32)
+    b = np.ldexp(b.astype(np.float64), x).astype(np.float32)
+    a = np.where(rng.random(n) < 0.5, a, -a).astype(np.float32)
+    sw = rng.random(n) < 0.5
+    a, b = np.where(sw, b, a).astype(np.float32), np.where(sw, a, b).astype(np.float32)
+    got = host(K.hypot_cr(dev(a), dev(b)))
+    want = np.empty_like(a)
+    ref.hypot_f32(a.ctypes.data, b.ctypes.data, want.ctypes.data, n)
+    _gen.assert_bits_equal(got, want, "hypotf near midpoints vs reference")
+    ex = np.array([_gen.hypot_exact(u, v, np.float32) for u, v in zip(a[:20000], b[:20000])], dtype=np.float32)
+    _gen.assert_bits_equal(got[:20000], ex, "hypotf near midpoints vs exact")
+
+
 @pytest.mark.parametrize("dt", DTS)
 def test_hypot_near_the_early_out(cuda, ref, dt):
     """Ratios small/big around kog2's widened early-out (2^-27 in double,
