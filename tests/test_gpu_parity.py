@@ -97,11 +97,44 @@ def test_hypot_exact_ties(cuda, dt):
     _gen.assert_bits_equal(got, ex, "hypot ties")
 
 
+def test_divf_near_midpoints(cuda):
+    """binary32 quotients as close to a rounding midpoint as 24-bit operands
+    allow: for an odd 25-bit M, Y = c M^-1 mod 2^25 (24 bits) makes
+    M Y = X 2^25 + c with |c| <= 8, so X 2^25 / Y lies c/(M Y) ~ 2^-49 .. 2^-45
+    (relative) from the midpoint M; a quotient approximation off by 2^-46
+    misrounds ~28% of them.  The unit kernel's div_rn<float>, which shares
+    div_mant_f (kog2_fp.cuh) with svd2's fast path, equals IEEE x / y."""
+    rng = np.random.default_rng(0xD21)
+    n = 4_000_000
+    mod = np.int64(1) << 25
+    M = rng.integers(1 << 24, 1 << 25, size=n, dtype=np.int64) | 1
+    inv = M.copy()
+    for _ in range(5):  # Newton's iteration for M^-1 mod 2^25
+        inv = (inv * ((2 - M * inv) % mod)) % mod
+    c = rng.integers(1, 9, size=n) * np.where(rng.random(n) < 0.5, 1, -1)
+    Y = (inv * (c % mod)) % mod
+    P = M * Y
+    ok = (Y >= 1 << 23) & (Y < 1 << 24) & (P - c >= np.int64(1) << 48)
+    Y, P, c = Y[ok], P[ok], c[ok]
+    X = (P - c) >> 25
+    assert ((X << 25) + c == P).all() and (X >= 1 << 23).all() and (X < 1 << 24).all() and X.size > 500_000
+    m = X.size
+    e = rng.integers(-60, 61, size=m)
+    x = np.ldexp(X.astype(np.float64), e + 2).astype(np.float32)
+    y = np.ldexp(Y.astype(np.float64), e - 23 - rng.integers(0, 8, size=m)).astype(np.float32)
+    x = np.where(rng.random(m) < 0.5, x, -x).astype(np.float32)
+    got = torch.empty(m, dtype=torch.float32, device="cuda")
+    dx, dy = dev(x), dev(y)
+    capi.check(capi.load().kog_div_batch_f32(dx.data_ptr(), dy.data_ptr(), got.data_ptr(), m,
+                                             torch.cuda.current_stream().cuda_stream))
+    _gen.assert_bits_equal(host(got), x / y, "binary32 division near midpoints")
+
+
 def test_hypotf_near_midpoints(cuda, ref):
     """binary32 hypot whose exact value lies 2^-58 .. 2^-41.6 (relative) from
     a rounding midpoint (28% below 2^-46, median 2^-44.8): either side of the
-    fast path's decision tolerance (kog2_fp.cuh hypot_main<float>).  m = M 2^-24 (M odd, 25 bits) is a
-    midpoint, a = (M - 1 - 2t) 2^-24 a float below it, and b the float
+    fast path's decision tolerance (kog2_fp.cuh hypot_main<float>).
+    m = M 2^-24 (M odd, 25 bits) is a midpoint, a = (M - 1 - 2t) 2^-24 a float below it, and b the float
     nearest sqrt(m^2 - a^2) moved by j ulps, so a^2 + b^2 - m^2 is about
     j 2^-24 of b^2.  Results equal the reference and the exact value."""
     rng = np.random.default_rng(0x68790005)
