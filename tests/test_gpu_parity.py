@@ -130,6 +130,61 @@ def test_divf_near_midpoints(cuda):
     _gen.assert_bits_equal(host(got), x / y, "binary32 division near midpoints")
 
 
+def test_divf_every_divisor_significand(cuda):
+    """Every binary32 divisor significand Y (2^23 of them) against a dividend
+    whose quotient lies next to a midpoint: with Y = 2^j Yo (Yo odd),
+    M = c' Yo^-1 mod 2^(25-j) lifted into [2^24, 2^25) makes M Y = X 2^25 + c,
+    c = c' 2^j, |c'| < 130 (found for 99.6% of the significands; the rest are
+    dropped).  This pins rcp_mant_f's single Newton step for every seed the
+    reciprocal instruction can see (kog2_fp.cuh)."""
+    rng = np.random.default_rng(0xD22)
+    Y = np.arange(1 << 23, 1 << 24, dtype=np.int64)
+    j = np.zeros_like(Y)
+    Yo = Y.copy()
+    for _ in range(23):
+        ev = (Yo & 1) == 0
+        Yo[ev] >>= 1
+        j[ev] += 1
+    mod = np.int64(1) << 25
+    inv = Yo.copy()
+    for _ in range(5):  # Newton's iteration for Yo^-1 mod 2^25
+        inv = (inv * ((2 - Yo * inv) % mod)) % mod
+    modj = np.int64(1) << (25 - j)
+    M = np.zeros_like(Y)
+    c = np.zeros_like(Y)
+    sgn = np.where(rng.random(Y.size) < 0.5, 1, -1)
+    todo = np.arange(Y.size)
+    for cp in range(1, 130, 2):
+        mj = modj[todo]
+        cs = cp * sgn[todo]
+        M0 = ((cs % mj) * inv[todo]) % mj
+        lo = ((np.int64(1) << 24) - M0 + mj - 1) // mj
+        hi = ((np.int64(1) << 25) - 1 - M0) // mj
+        t = np.minimum(lo + (rng.random(todo.size) * (hi - lo + 1)).astype(np.int64), hi)
+        ok = lo <= hi
+        M[todo[ok]] = (M0 + t * mj)[ok]
+        c[todo[ok]] = (cs << j[todo])[ok]
+        todo = todo[~ok]
+        if todo.size == 0:
+            break
+    keep = M != 0
+    assert keep.mean() > 0.99
+    M, c, Y = M[keep], c[keep], Y[keep]
+    P = M * Y
+    assert ((P - c) % mod == 0).all() and (M >= 1 << 24).all() and (M < 1 << 25).all() and (M & 1).all()
+    X = (P - c) >> 25
+    assert (X > 0).all() and (X < 1 << 24).all()
+    e = rng.integers(-60, 61, size=Y.size)
+    x = np.ldexp(X.astype(np.float64), e + 2).astype(np.float32)
+    y = np.ldexp(Y.astype(np.float64), e - 23).astype(np.float32)
+    x = np.where(rng.random(Y.size) < 0.5, x, -x).astype(np.float32)
+    got = torch.empty(Y.size, dtype=torch.float32, device="cuda")
+    dx, dy = dev(x), dev(y)
+    capi.check(capi.load().kog_div_batch_f32(dx.data_ptr(), dy.data_ptr(), got.data_ptr(), Y.size,
+                                             torch.cuda.current_stream().cuda_stream))
+    _gen.assert_bits_equal(host(got), x / y, "binary32 division, every divisor significand")
+
+
 def test_hypotf_near_midpoints(cuda, ref):
     """binary32 hypot whose exact value lies 2^-58 .. 2^-41.6 (relative) from
     a rounding midpoint (28% below 2^-46, median 2^-44.8): either side of the

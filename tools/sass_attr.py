@@ -68,6 +68,8 @@ tot = 0.0
 for a, n, t, src in ex:
     s = site.get(a - base, "?")
     op = src.split()[1] if src.startswith("@") else (src.split()[0] if src else "")
+    if os.environ.get("OPC") and not op.startswith(os.environ["OPC"]):  # OPC=DSETP: one opcode family only
+        continue
     c = agg[s]
     c["n"] += n
     c["t"] += t
