@@ -81,22 +81,7 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
   // 32-bit indices: n <= kFastChunk = 2^31 per launch, so i + stride < 2^32
   // (one 32x32->64 multiply-add per array address instead of 64-bit arithmetic)
   const unsigned n32 = static_cast<unsigned>(n), stride = gridDim.x * blockDim.x;
-#ifdef KOG2_FAST_PF
-  // lanes 0-3 prefetch the warp's next 32-entry tile of one input array each
-  // into L2 (one bulk prefetch per array; 16-byte aligned arrays only)
-  const T* pf = lane == 0 ? in.g11 : lane == 1 ? in.g12 : lane == 2 ? in.g21 : in.g22;
-  const bool pf_lane = lane < 4 && ((reinterpret_cast<uintptr_t>(in.g11) | reinterpret_cast<uintptr_t>(in.g12) |
-                                     reinterpret_cast<uintptr_t>(in.g21) | reinterpret_cast<uintptr_t>(in.g22)) & 15u) == 0;
-#endif
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n32; i += stride) {
-#ifdef KOG2_FAST_PF
-    {
-      const unsigned nxt = i - lane + stride;
-      if (pf_lane && nxt + 32u <= n32)  // n <= 2^31: no wrap-around
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf + nxt), "r"(32u * static_cast<unsigned>(sizeof(T)))
-                     : "memory");
-    }
-#endif
     const Mat<T> g{ld_cs(in.g11 + i), ld_cs(in.g12 + i), ld_cs(in.g21 + i), ld_cs(in.g22 + i)};
     Result<T> r;
     bool bad = false;
