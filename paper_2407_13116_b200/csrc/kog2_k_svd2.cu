@@ -74,8 +74,26 @@ __global__ void __launch_bounds__(kThreads, 3) k_svd2(InP<T> in, OutP<T> out, ui
 #ifndef KOG2_FAST_THREADS
 #define KOG2_FAST_THREADS 512  // 512 x 2 blocks/SM measured 0.5% faster than 256 x 4 (12.58 vs 12.64 ms per 2^28 cfg3)
 #endif
+// binary32 block shape: its kernel needs fewer registers than binary64's;
+// 512 x 3 blocks/SM (40 registers, a 24-byte spill) measured best on config 4
+// (8.89 ms per 2^28 against 8.92 for 384 x 4 and 256 x 5, 8.97 for 256 x 6,
+// 9.29 for 512 x 2; profiles/r9_ab_f32_shape.txt)
+#ifndef KOG2_F32_THREADS
+#define KOG2_F32_THREADS 512
+#endif
+#ifndef KOG2_F32_MINB
+#define KOG2_F32_MINB 3
+#endif
 template <class T>
-__global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
+struct FastShape {
+  static constexpr int threads = KOG2_FAST_THREADS, minb = KOG2_FAST_MINB;
+};
+template <>
+struct FastShape<float> {
+  static constexpr int threads = KOG2_F32_THREADS, minb = KOG2_F32_MINB;
+};
+template <class T>
+__global__ void __launch_bounds__(FastShape<T>::threads, FastShape<T>::minb)
     k_svd2_fast(InP<T> in, OutP<T> out, uint64_t n, uint32_t* list, unsigned* count) {
   const unsigned lane = threadIdx.x & 31u;
   // 32-bit indices: n <= kFastChunk = 2^31 per launch, so i + stride < 2^32
@@ -265,7 +283,8 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
                                                                                                sc->count);
         } else
 #endif
-          k_svd2_fast<T><<<grid_for(len, KOG2_FAST_THREADS), KOG2_FAST_THREADS, 0, st>>>(ip, ol, len, sc->list, sc->count);
+          k_svd2_fast<T><<<grid_for(len, FastShape<T>::threads), FastShape<T>::threads, 0, st>>>(ip, ol, len, sc->list,
+                                                                                           sc->count);
         if ((rc = launched("k_svd2_fast")) != KOG_OK) return rc;
         k_svd2_list<T><<<148 * 6, kThreads, 0, st>>>(ip, ol, sc->list, sc->count);
         if ((rc = launched("k_svd2_list")) != KOG_OK) return rc;
