@@ -476,6 +476,21 @@ def test_svd2_any_finite_all_options(cuda, ref, dt, opt):
     compare_svd(got, want, "svd2")
 
 
+def test_svd2_f32_secant_boundary(cuda, ref):
+    """binary32 svd2 whose tan(theta) = |g21| / |g11| lies in [2^-14, 2^-11]:
+    the fast path's sec_le1<float> (kog2_fast.cuh) returns 1 below 2^-12
+    and takes the root above; every field equals the reference's."""
+    n = 1 << 18
+    rng = np.random.default_rng(0x5EC1)
+    sgn = lambda: np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    g11 = sgn() * (1 + rng.random(n)) * np.exp2(rng.integers(-4, 5, n))
+    g21 = sgn() * np.abs(g11) * np.exp2(rng.uniform(-14, -11, n))
+    g12 = sgn() * (1 + rng.random(n)) * np.exp2(rng.integers(-9, -4, n)) * np.abs(g11)
+    g22 = sgn() * (1 + rng.random(n)) * np.exp2(rng.integers(-9, -4, n)) * np.abs(g11)
+    g = np.ascontiguousarray(np.stack([g11, g12, g21, g22]).astype(np.float32))
+    compare_svd(K.svd2(dev(g)), refbind.svd2(ref, g), "f32 secant boundary")
+
+
 TARGETED = [  # harness_test.cpp:181-193 + svd2_test.cpp known answers
     (1, 1, 0, 1), (2, 1, 0, 1), (4, 3, 0, 2), (1, 3, 0, 4), (2, 0, 0, 1), (3, 0, 4, 0), (1, 1, 0, 0),
     (1, 1, 1, -1), (2, 4, 1, 2), (0, 3, 2, 0), (-5, 0, 0, 0), (2, 1, 1, 2), (0, 2, 0, 1), (0, 0, 0, 0),
