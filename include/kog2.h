@@ -11,6 +11,11 @@
  *   - `*_batch_*` entry points take DEVICE pointers and a cudaStream_t passed as
  *     `void* stream` (NULL = legacy default stream); they are stream-ordered and
  *     do not synchronize; the caller owns every buffer;
+ *   - reentrant: any number of calls may be in flight at once on different
+ *     streams or host threads.  Internal scratch (deferred-lane lists, study
+ *     chunk buffers) is allocated per call on the caller's stream from a
+ *     per-device stream-ordered memory pool and freed on it after last use;
+ *     no call shares device scratch with another;
  *   - return value: KOG_OK (0) on success, a negative KOG_ERR_* code for an
  *     argument or CUDA error (message via kog_last_error()), or — for the
  *     routines whose reference throws std::domain_error — a positive count is
@@ -129,6 +134,16 @@ int kog_svd2_host_f64(const kog_mat_f64* in, const kog_svd_out_f64* out, uint64_
                       const kog_options* opt);
 int kog_svd2_host_f32(const kog_mat_f32* in, const kog_svd_out_f32* out, uint64_t n,
                       const kog_options* opt);
+
+/* Host-buffer forms of the per-matrix routines the C++ shim
+ * (include/kog2/kogsvd2_gpu.hpp) needs: each stages its arrays through device
+ * memory on a private stream and is synchronous.  hypot_cr (fpcore.hpp:140-188),
+ * svd2_ext (oracle.hpp:102-238), run_one's svd2 + svd2_ext + metrics
+ * (harness.hpp:190-222, oracle.hpp:269-301), generate (harness.hpp:139-186). */
+int kog_hypot_host_f64(const double* a, const double* b, double* out, uint64_t n);
+int kog_hypot_host_f32(const float* a, const float* b, float* out, uint64_t n);
+/* (kog_svd2_ext_host_*, kog_metrics_host_*, kog_generate_host_*: declared
+ * below, after their record types) */
 
 /* ------------------------------------------------ fpcore.hpp unit routines */
 /* hypot_cr<T> (fpcore.hpp:140-188) */
@@ -311,6 +326,13 @@ int kog_generate_batch_f64(const kog_run_config* cfg, uint64_t index0, const kog
                            uint64_t n, void* stream);
 int kog_generate_batch_f32(const kog_run_config* cfg, uint64_t index0, const kog_mat_f32* out,
                            uint64_t n, void* stream);
+/* host-buffer forms (synchronous; see kog_hypot_host_f64 above) */
+int kog_generate_host_f64(const kog_run_config* cfg, uint64_t index0, const kog_mat_f64* out, uint64_t n);
+int kog_generate_host_f32(const kog_run_config* cfg, uint64_t index0, const kog_mat_f32* out, uint64_t n);
+int kog_svd2_ext_host_f64(const kog_mat_f64* g, kog_extsvd* out, uint64_t n);
+int kog_svd2_ext_host_f32(const kog_mat_f32* g, kog_extsvd* out, uint64_t n);
+int kog_metrics_host_f64(const kog_mat_f64* g, kog_metrics* out, uint64_t n, const kog_options* opt);
+int kog_metrics_host_f32(const kog_mat_f32* g, kog_metrics* out, uint64_t n, const kog_options* opt);
 
 /* ErrorStats + BranchCounts (harness.hpp:50-106), plus the index at which the
  * max kappa was first attained (tie-break = reference merge order) and the
@@ -372,9 +394,10 @@ int kog_fp64_probe(double* sink, uint64_t threads, uint32_t iters, void* stream)
  * the general IEEE division out of line), exposed for verification. */
 int kog_div_batch_f64(const double* x, const double* y, double* out, uint64_t n, void* stream);
 int kog_div_batch_f32(const float* x, const float* y, float* out, uint64_t n, void* stream);
-/* Matrices of the last kog_svd2_batch_f64 launch pair (default Options) on the
- * current device and calling thread that left the specialised path and were
- * recomputed by the general kernel (synchronous; -1 if none ran yet). */
+/* Matrices that left the specialised path and were recomputed by the general
+ * kernel, summed over every kog_svd2_batch_* call (default Options) on the
+ * current device since the library was loaded (synchronous; -1 on error).
+ * Diagnostics only: take differences around the calls of interest. */
 int64_t kog_svd2_deferred_count(void);
 /* number of kernel launches issued by this library since load */
 uint64_t kog_launch_count(void);

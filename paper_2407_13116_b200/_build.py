@@ -35,7 +35,7 @@ CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math"
              f"-I{CUDA_HOME}/include", f"-I{ROOT}/include"]
 
 CU_SOURCES = ["kog2_k_svd2.cu", "kog2_k_units.cu", "kog2_k_study.cu"]
-CXX_SOURCES = ["kog2_host.cpp"]
+CXX_SOURCES = ["kog2_host.cpp", "kog2_ws.cpp"]
 HEADERS = [f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] if os.path.isdir(CSRC) else []
 
 

@@ -17,7 +17,7 @@ constexpr int kThreads = 256;
 // grid for an elementwise launch over n items (grid-stride loops inside)
 inline int grid_for(uint64_t n, int threads = kThreads) {
   uint64_t blocks = (n + threads - 1) / threads;
-  const uint64_t cap = 148ull * 64ull;
+  const uint64_t cap = static_cast<uint64_t>(kog2_sm_count()) * 64ull;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   return static_cast<int>(blocks);

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -177,22 +178,34 @@ struct Pool {
 std::mutex g_pool_mu;
 
 template <class T>
+void pool_release(Pool<T>& p) {
+  for (auto& s : p.slot) {
+    if (s.st) cudaStreamSynchronize(s.st), cudaStreamDestroy(s.st);
+    s.st = nullptr;
+    for (auto& b : s.in) cudaFree(b), b = nullptr;
+    for (auto& b : s.of) cudaFree(b), b = nullptr;
+    for (auto& b : s.oi) cudaFree(b), b = nullptr;
+    cudaFree(s.flags);
+    s.flags = nullptr;
+  }
+  p.ready = false;
+}
+
+template <class T>
 int pool_get(Pool<T>& p, int dev) {
   if (p.ready && p.dev == dev) return KOG_OK;
+  bool ok = true;
   for (auto& s : p.slot) {
-    if (cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking) != cudaSuccess)
-      return kog2_cuda_error("cudaStreamCreate");
-    for (auto& b : s.in)
-      if (cudaMalloc(reinterpret_cast<void**>(&b), kChunk * sizeof(T)) != cudaSuccess)
-        return kog2_cuda_error("cudaMalloc(pipeline in)");
-    for (auto& b : s.of)
-      if (cudaMalloc(reinterpret_cast<void**>(&b), kChunk * sizeof(T)) != cudaSuccess)
-        return kog2_cuda_error("cudaMalloc(pipeline out)");
-    for (auto& b : s.oi)
-      if (cudaMalloc(reinterpret_cast<void**>(&b), kChunk * sizeof(int32_t)) != cudaSuccess)
-        return kog2_cuda_error("cudaMalloc(pipeline out)");
-    if (cudaMalloc(reinterpret_cast<void**>(&s.flags), kChunk * sizeof(uint32_t)) != cudaSuccess)
-      return kog2_cuda_error("cudaMalloc(pipeline flags)");
+    ok = ok && cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking) == cudaSuccess;
+    for (auto& b : s.in) ok = ok && cudaMalloc(reinterpret_cast<void**>(&b), kChunk * sizeof(T)) == cudaSuccess;
+    for (auto& b : s.of) ok = ok && cudaMalloc(reinterpret_cast<void**>(&b), kChunk * sizeof(T)) == cudaSuccess;
+    for (auto& b : s.oi) ok = ok && cudaMalloc(reinterpret_cast<void**>(&b), kChunk * sizeof(int32_t)) == cudaSuccess;
+    ok = ok && cudaMalloc(reinterpret_cast<void**>(&s.flags), kChunk * sizeof(uint32_t)) == cudaSuccess;
+  }
+  if (!ok) {  // release whatever was created; the next call starts over
+    const int rc = kog2_cuda_error("svd2_host pipeline streams/buffers");
+    pool_release(p);
+    return rc;
   }
   p.dev = dev;
   p.ready = true;
@@ -216,12 +229,15 @@ int svd2_host(const MatC* in, const OutC* out, uint64_t n, const kog_options* op
   T* hof[6] = {out->sig1_f, out->sig2_f, out->u11, out->u12, out->v11, out->v12};
   int32_t* hoi[3] = {out->sig1_e, out->sig2_e, out->s};
   const uint64_t nchunks = (n + kChunk - 1) / kChunk;
-  for (uint64_t c = 0; c < nchunks; ++c) {
+  // every chunk's kernels take their deferral scratch per call on the slot's
+  // stream (kog2_ws.cpp), so overlapping slots share nothing but the device
+  for (uint64_t c = 0; c < nchunks && rc == KOG_OK; ++c) {
     Slot<T>& s = p.slot[c % kSlots];
     const uint64_t lo = c * kChunk, len = (n - lo < kChunk) ? n - lo : kChunk;
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < 4 && rc == KOG_OK; ++k)
       if (cudaMemcpyAsync(s.in[k], hin[k] + lo, len * sizeof(T), cudaMemcpyHostToDevice, s.st) != cudaSuccess)
-        return kog2_cuda_error("cudaMemcpyAsync H2D");
+        rc = kog2_cuda_error("cudaMemcpyAsync H2D");
+    if (rc != KOG_OK) break;
     MatC dm;
     dm.g11 = s.in[0];
     dm.g12 = s.in[1];
@@ -238,20 +254,114 @@ int svd2_host(const MatC* in, const OutC* out, uint64_t n, const kog_options* op
     dout.sig2_e = s.oi[1];
     dout.s = s.oi[2];
     dout.flags = s.flags;
-    rc = batch(&dm, &dout, len, opt, s.st);
-    if (rc != KOG_OK) return rc;
-    for (int k = 0; k < 6; ++k)
+    if ((rc = batch(&dm, &dout, len, opt, s.st)) != KOG_OK) break;
+    for (int k = 0; k < 6 && rc == KOG_OK; ++k)
       if (cudaMemcpyAsync(hof[k] + lo, s.of[k], len * sizeof(T), cudaMemcpyDeviceToHost, s.st) != cudaSuccess)
-        return kog2_cuda_error("cudaMemcpyAsync D2H");
-    for (int k = 0; k < 3; ++k)
+        rc = kog2_cuda_error("cudaMemcpyAsync D2H");
+    for (int k = 0; k < 3 && rc == KOG_OK; ++k)
       if (cudaMemcpyAsync(hoi[k] + lo, s.oi[k], len * sizeof(int32_t), cudaMemcpyDeviceToHost, s.st) != cudaSuccess)
-        return kog2_cuda_error("cudaMemcpyAsync D2H");
-    if (cudaMemcpyAsync(out->flags + lo, s.flags, len * sizeof(uint32_t), cudaMemcpyDeviceToHost, s.st) != cudaSuccess)
-      return kog2_cuda_error("cudaMemcpyAsync D2H");
+        rc = kog2_cuda_error("cudaMemcpyAsync D2H");
+    if (rc == KOG_OK &&
+        cudaMemcpyAsync(out->flags + lo, s.flags, len * sizeof(uint32_t), cudaMemcpyDeviceToHost, s.st) != cudaSuccess)
+      rc = kog2_cuda_error("cudaMemcpyAsync D2H");
   }
+  // drain every slot, also after an error: no copy into the caller's host
+  // buffers may still be running when this returns
   for (auto& s : p.slot)
-    if (cudaStreamSynchronize(s.st) != cudaSuccess) return kog2_cuda_error("cudaStreamSynchronize");
-  return KOG_OK;
+    if (cudaStreamSynchronize(s.st) != cudaSuccess && rc == KOG_OK) rc = kog2_cuda_error("cudaStreamSynchronize");
+  return rc;
+}
+
+// ------------------------------------- host-buffer forms of device routines
+// One staged call: device arrays from the workspace pool on a private stream,
+// H2D of the inputs, the device entry point, D2H of the outputs, synchronise.
+// Used by the per-matrix C++ shim (include/kog2/kogsvd2_gpu.hpp).
+struct HostArg {
+  const void* host;
+  size_t bytes;
+};
+struct HostOut {
+  void* host;
+  size_t bytes;
+};
+template <class F>
+int staged(std::initializer_list<HostArg> ins, std::initializer_list<HostOut> outs, F launch) {
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return kog2_cuda_error("cudaStreamCreate");
+  std::vector<void*> din, dout;
+  int rc = KOG_OK;
+  for (const HostArg& a : ins) {
+    void* d = kog2_ws_alloc(a.bytes, st);
+    if (!d) {
+      rc = KOG_ERR_CUDA;
+      break;
+    }
+    din.push_back(d);
+    if (cudaMemcpyAsync(d, a.host, a.bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+      rc = kog2_cuda_error("cudaMemcpyAsync H2D");
+      break;
+    }
+  }
+  for (size_t k = 0; rc == KOG_OK && k < outs.size(); ++k) {
+    void* d = kog2_ws_alloc(outs.begin()[k].bytes, st);
+    if (!d) rc = KOG_ERR_CUDA;
+    else dout.push_back(d);
+  }
+  if (rc == KOG_OK) rc = launch(din.data(), dout.data(), static_cast<void*>(st));
+  for (size_t k = 0; rc == KOG_OK && k < outs.size(); ++k)
+    if (cudaMemcpyAsync(outs.begin()[k].host, dout[k], outs.begin()[k].bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      rc = kog2_cuda_error("cudaMemcpyAsync D2H");
+  for (void* d : din) kog2_ws_free(d, st);
+  for (void* d : dout) kog2_ws_free(d, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && rc == KOG_OK) rc = kog2_cuda_error("cudaStreamSynchronize");
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+template <class T, class MatC>
+int hypot_host(const T* a, const T* b, T* out, uint64_t n, int (*fn)(const T*, const T*, T*, uint64_t, void*)) {
+  if (n == 0) return KOG_OK;
+  if (!a || !b || !out) return kog2_arg_error("kog_hypot_host: null argument");
+  const size_t B = n * sizeof(T);
+  return staged({{a, B}, {b, B}}, {{out, B}}, [&](void** di, void** dout, void* st) {
+    return fn(static_cast<const T*>(di[0]), static_cast<const T*>(di[1]), static_cast<T*>(dout[0]), n, st);
+  });
+}
+
+template <class T, class MatC>
+MatC mat_of(void** d) {
+  MatC m;
+  m.g11 = static_cast<T*>(d[0]);
+  m.g12 = static_cast<T*>(d[1]);
+  m.g21 = static_cast<T*>(d[2]);
+  m.g22 = static_cast<T*>(d[3]);
+  return m;
+}
+
+template <class T, class MatC, class Rec, class F>
+int per_matrix_host(const MatC* g, Rec* out, uint64_t n, F fn) {
+  if (n == 0) return KOG_OK;
+  if (!g || !g->g11 || !g->g12 || !g->g21 || !g->g22 || !out) return kog2_arg_error("kog host call: null argument");
+  const size_t B = n * sizeof(T);
+  return staged({{g->g11, B}, {g->g12, B}, {g->g21, B}, {g->g22, B}}, {{out, n * sizeof(Rec)}},
+                [&](void** di, void** dout, void* st) {
+                  const MatC m = mat_of<T, MatC>(di);
+                  return fn(&m, static_cast<Rec*>(dout[0]), st);
+                });
+}
+
+template <class T, class MatC>
+int generate_host(const kog_run_config* cfg, uint64_t index0, const MatC* out, uint64_t n,
+                  int (*fn)(const kog_run_config*, uint64_t, const MatC*, uint64_t, void*)) {
+  if (n == 0) return KOG_OK;
+  if (!cfg || !out || !out->g11 || !out->g12 || !out->g21 || !out->g22)
+    return kog2_arg_error("kog_generate_host: null argument");
+  const size_t B = n * sizeof(T);
+  return staged({}, {{out->g11, B}, {out->g12, B}, {out->g21, B}, {out->g22, B}},
+                [&](void**, void** dout, void* st) {
+                  const MatC m = mat_of<T, MatC>(dout);
+                  return fn(cfg, index0, &m, n, st);
+                });
 }
 
 template <class T>
@@ -302,6 +412,39 @@ int kog_svd2_host_f64(const kog_mat_f64* in, const kog_svd_out_f64* out, uint64_
 }
 int kog_svd2_host_f32(const kog_mat_f32* in, const kog_svd_out_f32* out, uint64_t n, const kog_options* opt) {
   return svd2_host<float>(in, out, n, opt, &kog_svd2_batch_f32);
+}
+
+int kog_hypot_host_f64(const double* a, const double* b, double* out, uint64_t n) {
+  return hypot_host<double, kog_mat_f64>(a, b, out, n, &kog_hypot_batch_f64);
+}
+int kog_hypot_host_f32(const float* a, const float* b, float* out, uint64_t n) {
+  return hypot_host<float, kog_mat_f32>(a, b, out, n, &kog_hypot_batch_f32);
+}
+int kog_svd2_ext_host_f64(const kog_mat_f64* g, kog_extsvd* out, uint64_t n) {
+  return per_matrix_host<double>(g, out, n, [&](const kog_mat_f64* m, kog_extsvd* o, void* st) {
+    return kog_svd2_ext_batch_f64(m, o, n, st);
+  });
+}
+int kog_svd2_ext_host_f32(const kog_mat_f32* g, kog_extsvd* out, uint64_t n) {
+  return per_matrix_host<float>(g, out, n, [&](const kog_mat_f32* m, kog_extsvd* o, void* st) {
+    return kog_svd2_ext_batch_f32(m, o, n, st);
+  });
+}
+int kog_metrics_host_f64(const kog_mat_f64* g, kog_metrics* out, uint64_t n, const kog_options* opt) {
+  return per_matrix_host<double>(g, out, n, [&](const kog_mat_f64* m, kog_metrics* o, void* st) {
+    return kog_metrics_batch_f64(m, o, n, opt, st);
+  });
+}
+int kog_metrics_host_f32(const kog_mat_f32* g, kog_metrics* out, uint64_t n, const kog_options* opt) {
+  return per_matrix_host<float>(g, out, n, [&](const kog_mat_f32* m, kog_metrics* o, void* st) {
+    return kog_metrics_batch_f32(m, o, n, opt, st);
+  });
+}
+int kog_generate_host_f64(const kog_run_config* cfg, uint64_t index0, const kog_mat_f64* out, uint64_t n) {
+  return generate_host<double>(cfg, index0, out, n, &kog_generate_batch_f64);
+}
+int kog_generate_host_f32(const kog_run_config* cfg, uint64_t index0, const kog_mat_f32* out, uint64_t n) {
+  return generate_host<float>(cfg, index0, out, n, &kog_generate_batch_f32);
 }
 
 void kog_stats_init(kog_stats* st) {

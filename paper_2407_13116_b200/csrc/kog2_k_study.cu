@@ -394,21 +394,11 @@ int launch_ext(const MatC* g, kog_extsvd* o, uint64_t n, cudaStream_t st) {
 
 
 // ------------------------------------------------------------ study launcher
-// Per device and host thread: the per-block (kappa, index) slots and, for the
-// phased kog study, one chunk of generated matrices and their decompositions.
-struct StudyScratch {
-  BlockPartial* part = nullptr;
-  int blocks = 0;
-  void* buf = nullptr;
-  size_t cap = 0;
-  // phased study pipeline: a producer stream (generate + svd2, whose deferral
-  // scratch is single-user) and two consumer streams (reference sigma +
-  // metrics) over two chunk buffers; events chain them
-  cudaStream_t prod = nullptr, cons[2] = {nullptr, nullptr};
-  cudaEvent_t ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr}, join[3] = {nullptr, nullptr, nullptr},
-              fork = nullptr;
-};
-thread_local StudyScratch g_study[64];
+// Every call owns its scratch: the per-block (kappa, index) slots and, for the
+// phased kog study, two chunks of generated matrices and their decompositions
+// come from the stream-ordered workspace pool (kog2_ws.cpp) on the caller's
+// stream and go back to it after the join, so studies on different streams or
+// threads never share a buffer.
 
 #ifndef KOG2_STUDY_STREAMS_DEFAULT
 #define KOG2_STUDY_STREAMS_DEFAULT 1  // two consumer streams ran two k_study at once: erratic 500-1500 M/s at 2^31
@@ -443,30 +433,6 @@ int study_bps() {
   return v;
 }
 
-int study_streams(StudyScratch& sc) {
-  if (sc.prod) return KOG_OK;
-  bool ok = cudaStreamCreateWithFlags(&sc.prod, cudaStreamNonBlocking) == cudaSuccess;
-  for (int k = 0; k < 2; ++k) {
-    ok = ok && cudaStreamCreateWithFlags(&sc.cons[k], cudaStreamNonBlocking) == cudaSuccess;
-    ok = ok && cudaEventCreateWithFlags(&sc.ready[k], cudaEventDisableTiming) == cudaSuccess;
-    ok = ok && cudaEventCreateWithFlags(&sc.freed[k], cudaEventDisableTiming) == cudaSuccess;
-  }
-  for (int k = 0; k < 3; ++k) ok = ok && cudaEventCreateWithFlags(&sc.join[k], cudaEventDisableTiming) == cudaSuccess;
-  ok = ok && cudaEventCreateWithFlags(&sc.fork, cudaEventDisableTiming) == cudaSuccess;
-  return ok ? KOG_OK : kog2_cuda_error("study streams/events");
-}
-
-int study_partials(StudyScratch& sc, int grid) {
-  if (sc.blocks >= grid) return KOG_OK;
-  if (sc.part) cudaFree(sc.part);
-  sc.part = nullptr;
-  sc.blocks = 0;
-  if (cudaMalloc(reinterpret_cast<void**>(&sc.part), sizeof(BlockPartial) * grid) != cudaSuccess)
-    return kog2_cuda_error("cudaMalloc(study partials)");
-  sc.blocks = grid;
-  return KOG_OK;
-}
-
 constexpr uint64_t kStudyChunk = 1ull << 22;
 
 template <class T> struct Abi;
@@ -498,21 +464,47 @@ template <> struct Abi<float> {
 // instruction fetch: ~85% "no instruction" stalls), and the buffers cost
 // ~200 B of HBM traffic per matrix.
 template <class T>
-int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats, StudyScratch& sc, int sms,
-                 cudaStream_t st) {
+int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats, int sms,
+                     cudaStream_t st, uint64_t C, int nbuf, size_t per, int gmax, char* ws, BlockPartial* part,
+                     Kog2SideStreams* side);
+template <class T>
+int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats, int sms, cudaStream_t st) {
   const uint64_t C = n < kStudyChunk ? n : kStudyChunk;
   const int nbuf = n > C ? 2 : 1;  // two chunk buffers when there is more than one chunk
   const size_t per = static_cast<size_t>(C) * (6 * 8 + 10 * sizeof(T) + 4 * sizeof(int32_t));
-  const size_t need = per * nbuf;
-  if (sc.cap < need) {
-    if (sc.buf) cudaFree(sc.buf);
-    sc.buf = nullptr;
-    sc.cap = 0;
-    if (cudaMalloc(&sc.buf, need) != cudaSuccess) return kog2_cuda_error("cudaMalloc(study chunk)");
-    sc.cap = need;
+  const int gmax = study_grid(C, sms, study_bps());
+  // one set of per-block kappa slots per consumer stream (concurrent k_study
+  // launches never share a slot) after the chunk buffers
+  const size_t part_off = (per * nbuf + 255) / 256 * 256;
+  const size_t need = part_off + sizeof(BlockPartial) * 2 * gmax;
+  char* ws = static_cast<char*>(kog2_ws_alloc(need, st));
+  if (!ws) return KOG_ERR_CUDA;
+  BlockPartial* part = reinterpret_cast<BlockPartial*>(ws + part_off);
+  Kog2SideStreams* side = kog2_side_acquire();
+  if (!side) {
+    kog2_ws_free(ws, st);
+    return KOG_ERR_CUDA;
   }
-  int rc = study_streams(sc);
-  if (rc != KOG_OK) return rc;
+  const int rc = study_phased_run<T>(cfg, index0, n, stats, sms, st, C, nbuf, per, gmax, ws, part, side);
+  // the join (inside) has ordered every side-stream use of ws before this free
+  const int frc = kog2_ws_free(ws, st);
+  kog2_side_release(side);
+  return rc != KOG_OK ? rc : frc;
+}
+
+template <class T>
+int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats, int sms,
+                     cudaStream_t st, uint64_t C, int nbuf, size_t per, int gmax, char* ws, BlockPartial* part,
+                     Kog2SideStreams* side) {
+  int rc = KOG_OK;
+  const cudaStream_t s_prod = static_cast<cudaStream_t>(side->st[0]);
+  const cudaStream_t s_cons[2] = {static_cast<cudaStream_t>(side->st[1]), static_cast<cudaStream_t>(side->st[2])};
+  cudaEvent_t ev[8];
+  for (int k = 0; k < 8; ++k) ev[k] = static_cast<cudaEvent_t>(side->ev[k]);
+  cudaEvent_t* ready = ev;      // [2]
+  cudaEvent_t* freed = ev + 2;  // [2]
+  cudaEvent_t* join = ev + 4;   // [3]
+  cudaEvent_t fork = ev[7];
   struct Bufs {
     typename Abi<T>::Mat gm;
     typename Abi<T>::Out om;
@@ -520,7 +512,7 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
     SvdBuf<T> sb;
   } bufs[2];
   for (int k = 0; k < nbuf; ++k) {
-    double* rd = reinterpret_cast<double*>(static_cast<char*>(sc.buf) + per * k);  // the 8-byte arrays first
+    double* rd = reinterpret_cast<double*>(ws + per * k);  // the 8-byte arrays first
     long long* rq = reinterpret_cast<long long*>(rd);
     T* t = reinterpret_cast<T*>(rd + 6 * C);
     int32_t* w = reinterpret_cast<int32_t*>(t + 10 * C);
@@ -532,50 +524,60 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
     bufs[k].sb = SvdBuf<T>{om.sig1_f, om.sig2_f, om.sig1_e, om.sig2_e, om.u11, om.u12, om.v11,
                            om.v12,    om.flags,  rq,        rq + C,    rd + 2 * C, rd + 3 * C, rd + 4 * C, rd + 5 * C};
   }
-  const int gmax = study_grid(C, sms, study_bps());
-  // one set of per-block kappa slots per consumer stream (concurrent k_study
-  // launches never share a slot); every slot starts empty, each chunk's blocks
-  // merge into their own slot, and k_study_finish merges all slots at the end
-  if ((rc = study_partials(sc, 2 * gmax)) != KOG_OK) return rc;
-  if (cudaMemsetAsync(sc.part, 0, sizeof(BlockPartial) * 2 * gmax, st) != cudaSuccess)
+  // every slot starts empty, each chunk's blocks merge into their own slot,
+  // and k_study_finish merges all slots at the end
+  if (cudaMemsetAsync(part, 0, sizeof(BlockPartial) * 2 * gmax, st) != cudaSuccess)
     return kog2_cuda_error("cudaMemsetAsync(study partials)");
   // fork from the caller's stream
   const int mode = study_streams_mode();
-  const cudaStream_t prod = mode == 0 ? st : sc.prod;
-  const cudaStream_t cons[2] = {mode == 0 ? st : sc.cons[0], mode == 2 ? sc.cons[1] : (mode == 0 ? st : sc.cons[0])};
-  if (cudaEventRecord(sc.fork, st) != cudaSuccess || cudaStreamWaitEvent(sc.prod, sc.fork, 0) != cudaSuccess ||
-      cudaStreamWaitEvent(sc.cons[0], sc.fork, 0) != cudaSuccess ||
-      cudaStreamWaitEvent(sc.cons[1], sc.fork, 0) != cudaSuccess)
+  const cudaStream_t prod = mode == 0 ? st : s_prod;
+  const cudaStream_t cons[2] = {mode == 0 ? st : s_cons[0], mode == 2 ? s_cons[1] : (mode == 0 ? st : s_cons[0])};
+  if (cudaEventRecord(fork, st) != cudaSuccess || cudaStreamWaitEvent(s_prod, fork, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(s_cons[0], fork, 0) != cudaSuccess || cudaStreamWaitEvent(s_cons[1], fork, 0) != cudaSuccess)
     return kog2_cuda_error("study fork");
+  // on an error after the fork, the join below still runs, so nothing enqueued
+  // on a side stream can outlive the workspace freed on st by the caller
   uint64_t c = 0;
-  for (uint64_t lo = 0; lo < n; lo += C, ++c) {
+  for (uint64_t lo = 0; lo < n && rc == KOG_OK; lo += C, ++c) {
     const uint64_t len = n - lo < C ? n - lo : C;
     const int k = static_cast<int>(c & 1);
     Bufs& bf = bufs[nbuf == 2 ? k : 0];
     cudaStream_t q = cons[k];
     // producer: generate + svd2 into buffer k once its previous consumer is done
-    if (c >= 2 && cudaStreamWaitEvent(prod, sc.freed[k], 0) != cudaSuccess) return kog2_cuda_error("study wait");
-    if ((rc = Abi<T>::gen(cfg, index0 + lo, &bf.gm, len, prod)) != KOG_OK) return rc;
-    if ((rc = Abi<T>::svd(&bf.gm, &bf.om, len, &cfg->options, prod)) != KOG_OK) return rc;
+    if (c >= 2 && cudaStreamWaitEvent(prod, freed[k], 0) != cudaSuccess) {
+      rc = kog2_cuda_error("study wait");
+      break;
+    }
+    if ((rc = Abi<T>::gen(cfg, index0 + lo, &bf.gm, len, prod)) != KOG_OK) break;
+    if ((rc = Abi<T>::svd(&bf.gm, &bf.om, len, &cfg->options, prod)) != KOG_OK) break;
     // consumer k: reference sigma + metrics + ErrorStats
-    if (cudaEventRecord(sc.ready[k], prod) != cudaSuccess || cudaStreamWaitEvent(q, sc.ready[k], 0) != cudaSuccess)
-      return kog2_cuda_error("study chunk handoff");
+    if (cudaEventRecord(ready[k], prod) != cudaSuccess || cudaStreamWaitEvent(q, ready[k], 0) != cudaSuccess) {
+      rc = kog2_cuda_error("study chunk handoff");
+      break;
+    }
 #ifdef KOG2_STUDY_REF_KERNEL  // (the separate reference-sigma pass, for A/B)
     k_ref_sigma<T><<<grid_for(len), kThreads, 0, q>>>(bf.gin, bf.sb, len);
-    if ((rc = launched("k_ref_sigma")) != KOG_OK) return rc;
+    if ((rc = launched("k_ref_sigma")) != KOG_OK) break;
 #endif
     const int grid = study_grid(len, sms, study_bps());
     k_study<T, KOG_ROUTINE_KOG, true><<<grid, kStudyThreads, 0, q>>>(GenCfg{}, index0 + lo, len, Opt{}, stats,
-                                                                   sc.part + k * gmax, bf.gin, bf.sb, true);
-    if ((rc = launched("k_study")) != KOG_OK) return rc;
-    if (cudaEventRecord(sc.freed[k], q) != cudaSuccess) return kog2_cuda_error("study chunk release");
+                                                                   part + k * gmax, bf.gin, bf.sb, true);
+    if ((rc = launched("k_study")) != KOG_OK) break;
+    if (cudaEventRecord(freed[k], q) != cudaSuccess) {
+      rc = kog2_cuda_error("study chunk release");
+      break;
+    }
   }
   // join back into the caller's stream
-  const cudaStream_t sides[3] = {sc.prod, sc.cons[0], sc.cons[1]};
+  const cudaStream_t sides[3] = {s_prod, s_cons[0], s_cons[1]};
   for (int k = 0; k < 3; ++k)
-    if (cudaEventRecord(sc.join[k], sides[k]) != cudaSuccess || cudaStreamWaitEvent(st, sc.join[k], 0) != cudaSuccess)
-      return kog2_cuda_error("study join");
-  k_study_finish<<<1, kThreads, 0, st>>>(stats, sc.part, 2 * gmax);
+    if (cudaEventRecord(join[k], sides[k]) != cudaSuccess || cudaStreamWaitEvent(st, join[k], 0) != cudaSuccess) {
+      // cannot order the side streams before the caller's free: drain them
+      for (auto q : sides) cudaStreamSynchronize(q);
+      return rc != KOG_OK ? rc : kog2_cuda_error("study join");
+    }
+  if (rc != KOG_OK) return rc;
+  k_study_finish<<<1, kThreads, 0, st>>>(stats, part, 2 * gmax);
   return launched("k_study_finish");
 }
 
@@ -619,28 +621,29 @@ int kog_study_batch(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_
   if (!cfg || !stats_dev) return kog2_arg_error("kog_study_batch: null argument");
   if (kog_validate(cfg) != KOG_OK) return KOG_ERR_ARG;
   if (n == 0) return KOG_OK;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kog2_cuda_error("cudaGetDevice");
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  StudyScratch& sc = g_study[dev];
+  const int sms = kog2_sm_count();
   cudaStream_t st = KOG2_ST(stream);
   if (cfg->routine == KOG_ROUTINE_KOG)
-    return cfg->single_precision ? study_phased<float>(cfg, index0, n, stats_dev, sc, sms, st)
-                                 : study_phased<double>(cfg, index0, n, stats_dev, sc, sms, st);
+    return cfg->single_precision ? study_phased<float>(cfg, index0, n, stats_dev, sms, st)
+                                 : study_phased<double>(cfg, index0, n, stats_dev, sms, st);
+  // the lasv2 routine: one fused kernel over the range, per-call block slots
   const int grid = study_grid(n, sms);
-  int rc = study_partials(sc, grid);
-  if (rc != KOG_OK) return rc;
+  BlockPartial* part = static_cast<BlockPartial*>(kog2_ws_alloc(sizeof(BlockPartial) * grid, st));
+  if (!part) return KOG_ERR_CUDA;
   const Opt o = opt_of(&cfg->options);
   if (cfg->single_precision)
     k_study<float, KOG_ROUTINE_LASV2, false><<<grid, kStudyThreads, 0, st>>>(gen_cfg_of<float>(cfg), index0, n, o, stats_dev,
-                                                                         sc.part, InP<float>{}, SvdBuf<float>{}, false);
+                                                                         part, InP<float>{}, SvdBuf<float>{}, false);
   else
     k_study<double, KOG_ROUTINE_LASV2, false><<<grid, kStudyThreads, 0, st>>>(gen_cfg_of<double>(cfg), index0, n, o, stats_dev,
-                                                                          sc.part, InP<double>{}, SvdBuf<double>{}, false);
-  if ((rc = launched("k_study")) != KOG_OK) return rc;
-  k_study_finish<<<1, kThreads, 0, st>>>(stats_dev, sc.part, grid);
-  return launched("k_study_finish");
+                                                                          part, InP<double>{}, SvdBuf<double>{}, false);
+  int rc = launched("k_study");
+  if (rc == KOG_OK) {
+    k_study_finish<<<1, kThreads, 0, st>>>(stats_dev, part, grid);
+    rc = launched("k_study_finish");
+  }
+  const int frc = kog2_ws_free(part, st);
+  return rc != KOG_OK ? rc : frc;
 }
 
 }  // extern "C"

@@ -207,11 +207,16 @@ bool tma_ok(const InP<T>& ip) {
 }
 #endif
 
+// matrices recomputed by k_svd2_list on this device since load (diagnostics:
+// kog_svd2_deferred_count)
+__device__ unsigned long long g_kog2_deferred_total = 0;
+
 // the general algorithm over the deferred indices (gathered loads/stores)
 template <class T>
 __global__ void __launch_bounds__(kThreads, 3)
     k_svd2_list(InP<T> in, OutP<T> out, const uint32_t* list, const unsigned* count) {
   const uint64_t cnt = *count;
+  if (cnt && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_kog2_deferred_total, static_cast<unsigned long long>(cnt));
   for (uint64_t k = gtid(); k < cnt; k += gstride()) {
     const uint64_t i = list[k];
     const Mat<T> g{in.g11[i], in.g12[i], in.g21[i], in.g22[i]};
@@ -219,33 +224,6 @@ __global__ void __launch_bounds__(kThreads, 3)
     svd2<T>(g, opt_default(), r);
     store_result(out, i, r);
   }
-}
-
-// per-device deferred-index scratch (grown on demand; one per host thread so
-// concurrent callers on different threads never share it)
-struct Scratch {
-  uint32_t* list = nullptr;
-  unsigned* count = nullptr;
-  uint64_t cap = 0;
-};
-
-thread_local Scratch g_scratch[64];
-
-int scratch_for(uint64_t n, Scratch*& sc) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kog2_cuda_error("cudaGetDevice");
-  sc = &g_scratch[dev];
-  if (sc->cap >= n && sc->count) return KOG_OK;
-  if (sc->list) cudaFree(sc->list);
-  if (!sc->count && cudaMalloc(reinterpret_cast<void**>(&sc->count), sizeof(unsigned)) != cudaSuccess)
-    return kog2_cuda_error("cudaMalloc(defer count)");
-  if (cudaMalloc(reinterpret_cast<void**>(&sc->list), n * sizeof(uint32_t)) != cudaSuccess) {
-    sc->list = nullptr;
-    sc->cap = 0;
-    return kog2_cuda_error("cudaMalloc(defer list)");
-  }
-  sc->cap = n;
-  return KOG_OK;
 }
 
 constexpr uint64_t kFastChunk = 1ull << 31;  // uint32 deferred indices per launch pair
@@ -263,33 +241,45 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
   static const bool general_only = std::getenv("KOG2_SVD2_GENERAL") != nullptr;  // A/B comparisons
   {
     if (opt_is_default(o) && !general_only) {
-      Scratch* sc = nullptr;
-      int rc = scratch_for(n < kFastChunk ? n : kFastChunk, sc);
-      if (rc != KOG_OK) return rc;
-      for (uint64_t lo = 0; lo < n; lo += kFastChunk) {
+      // per-call deferral scratch, stream-ordered from the workspace pool: the
+      // count (first 256 bytes) and one index per matrix of the largest launch
+      // (4 B/matrix against the caller's 96, or 56 for binary32)
+      const uint64_t cap = n < kFastChunk ? n : kFastChunk;
+      char* ws = static_cast<char*>(kog2_ws_alloc(256 + cap * sizeof(uint32_t), st));
+      if (!ws) return KOG_ERR_CUDA;
+      unsigned* count = reinterpret_cast<unsigned*>(ws);
+      uint32_t* list = reinterpret_cast<uint32_t*>(ws + 256);
+      const int sms = kog2_sm_count();
+      int rc = KOG_OK;
+      for (uint64_t lo = 0; lo < n && rc == KOG_OK; lo += kFastChunk) {
         const uint64_t len = n - lo < kFastChunk ? n - lo : kFastChunk;
         const InP<T> ip{in->g11 + lo, in->g12 + lo, in->g21 + lo, in->g22 + lo};
         const OutP<T> ol{op.sig1_f + lo, op.sig2_f + lo, op.sig1_e + lo, op.sig2_e + lo, op.u11 + lo,
                          op.u12 + lo,    op.v11 + lo,    op.v12 + lo,    op.s + lo,      op.flags + lo};
-        if (cudaMemsetAsync(sc->count, 0, sizeof(unsigned), st) != cudaSuccess)
-          return kog2_cuda_error("cudaMemsetAsync(defer count)");
+        if (cudaMemsetAsync(count, 0, sizeof(unsigned), st) != cudaSuccess) {
+          rc = kog2_cuda_error("cudaMemsetAsync(defer count)");
+          break;
+        }
 #ifdef KOG2_FAST_TMA
         if (tma_ok(ip)) {
           constexpr int smem = (KOG2_FAST_THREADS / 32) * sizeof(TmaSlot<T>);
           static const bool attr = cudaFuncSetAttribute(k_svd2_fast_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                         smem) == cudaSuccess;
           (void)attr;
-          k_svd2_fast_tma<T><<<grid_for(len, KOG2_FAST_THREADS), KOG2_FAST_THREADS, smem, st>>>(ip, ol, len, sc->list,
-                                                                                               sc->count);
+          k_svd2_fast_tma<T><<<grid_for(len, KOG2_FAST_THREADS), KOG2_FAST_THREADS, smem, st>>>(ip, ol, len, list,
+                                                                                               count);
         } else
 #endif
-          k_svd2_fast<T><<<grid_for(len, FastShape<T>::threads), FastShape<T>::threads, 0, st>>>(ip, ol, len, sc->list,
-                                                                                           sc->count);
-        if ((rc = launched("k_svd2_fast")) != KOG_OK) return rc;
-        k_svd2_list<T><<<148 * 6, kThreads, 0, st>>>(ip, ol, sc->list, sc->count);
-        if ((rc = launched("k_svd2_list")) != KOG_OK) return rc;
+          k_svd2_fast<T><<<grid_for(len, FastShape<T>::threads), FastShape<T>::threads, 0, st>>>(ip, ol, len, list,
+                                                                                           count);
+        if ((rc = launched("k_svd2_fast")) != KOG_OK) break;
+        // deferred lanes are rare (none in 2^22-matrix samples of configs 1-5):
+        // two blocks per SM drain a list of any length (grid-stride)
+        k_svd2_list<T><<<2 * sms, kThreads, 0, st>>>(ip, ol, list, count);
+        rc = launched("k_svd2_list");
       }
-      return KOG_OK;
+      const int frc = kog2_ws_free(ws, st);
+      return rc != KOG_OK ? rc : frc;
     }
   }
   const int grid = grid_for(n);
@@ -324,12 +314,11 @@ int kog2_fast_stats(unsigned long long* out, int reset) {
 #endif
 
 int64_t kog_svd2_deferred_count(void) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
-  const Scratch* sc = &g_scratch[dev];
-  if (!sc->count) return -1;
-  unsigned c = 0;
-  if (cudaMemcpy(&c, sc->count, sizeof c, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  unsigned long long c = 0;
+  if (cudaMemcpyFromSymbol(&c, g_kog2_deferred_total, sizeof c) != cudaSuccess) {
+    kog2_cuda_error("cudaMemcpyFromSymbol(deferred total)");
+    return -1;
+  }
   return static_cast<int64_t>(c);
 }
 

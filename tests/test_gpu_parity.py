@@ -185,6 +185,56 @@ def test_divf_every_divisor_significand(cuda):
     _gen.assert_bits_equal(host(got), x / y, "binary32 division, every divisor significand")
 
 
+def _subnormal_tie_quotients(rng, n: int):
+    """binary32 pairs whose exact quotient is a subnormal midpoint k 2^-150
+    (k odd, up to 2^23 + ...), e.g. 0x1.74d94ap-101 / 0x1.f121b8p+47 = 3 2^-150:
+    y = Y 2^ey, x = k Y 2^(ey-150) with k Y < 2^24.  Half of them are nudged to
+    the neighbouring dividend (x +- 1 ulp), which lies just off the tie."""
+    kbits = rng.integers(1, 24, size=n)
+    k = (rng.integers(0, 1 << 62, size=n) >> (62 - kbits)) | 1
+    ybits = 24 - np.ceil(np.log2(k + 1)).astype(np.int64)
+    Y = np.maximum(rng.integers(0, 1 << 62, size=n) >> (62 - np.maximum(ybits, 1)), 1)
+    Y = np.where(k * Y < (1 << 24), Y, 1)
+    ey = rng.integers(1, 128 - 24, size=n)  # x on the binary32 grid: ey - 150 >= -149
+    y = np.ldexp(Y.astype(np.float64), ey).astype(np.float32)
+    x = np.ldexp((k * Y).astype(np.float64), ey - 150).astype(np.float32)
+    assert (np.ldexp((k * Y).astype(np.float64), ey - 150) == x.astype(np.float64)).all()
+    nudge = rng.random(n) < 0.5
+    x = np.where(nudge, np.nextafter(x, np.where(rng.random(n) < 0.5, np.float32(0), np.float32(1))), x)
+    sgn = np.where(rng.random(n) < 0.5, np.float32(1), np.float32(-1))
+    return (x * sgn).astype(np.float32), np.where(rng.random(n) < 0.5, y, -y).astype(np.float32)
+
+
+def test_divf_subnormal_ties(cuda):
+    """binary32 quotients that are exact subnormal midpoints (round half to
+    even on the 2^-149 grid) and their neighbours: div_rn<float> (quot_f's
+    residual step, kog2_fp.cuh) equals IEEE x / y."""
+    rng = np.random.default_rng(0xD23)
+    x, y = _subnormal_tie_quotients(rng, 1 << 20)
+    ties = (np.abs(x.astype(np.float64) / y.astype(np.float64)) < 2.0 ** -126)
+    assert ties.mean() > 0.9
+    got = torch.empty(x.size, dtype=torch.float32, device="cuda")
+    dx, dy = dev(x), dev(y)
+    capi.check(capi.load().kog_div_batch_f32(dx.data_ptr(), dy.data_ptr(), got.data_ptr(), x.size,
+                                             torch.cuda.current_stream().cuda_stream))
+    _gen.assert_bits_equal(host(got), x / y, "binary32 subnormal tie quotients")
+
+
+def test_svd2_f32_subnormal_tan_theta(cuda, ref):
+    """binary32 svd2 whose tan(theta) = |g21| / |g11| is an exact subnormal
+    midpoint (or next to one): the fast path's div_n<float> and the general
+    kernel's div_rn<float> (every Options combination) equal the reference."""
+    rng = np.random.default_rng(0x5B7)
+    n = 1 << 18
+    x, y = _subnormal_tie_quotients(rng, n)
+    y = np.where(np.abs(y) < 2.0 ** -100, np.float32(1.5), y).astype(np.float32)
+    small = lambda: (np.where(rng.random(n) < 0.5, -1.0, 1.0) * (1 + rng.random(n))
+                     * np.exp2(rng.integers(-40, -20, n)) * np.abs(y.astype(np.float64))).astype(np.float32)
+    g = np.ascontiguousarray(np.stack([y, small(), x, small()]).astype(np.float32))
+    for o in ALL_OPTIONS:
+        compare_svd(K.svd2(dev(g), K_opt(o)), refbind.svd2(ref, g, o), f"f32 subnormal tan(theta) {K_opt(o)}")
+
+
 def test_hypotf_near_midpoints(cuda, ref):
     """binary32 hypot whose exact value lies 2^-58 .. 2^-41.6 (relative) from
     a rounding midpoint (28% below 2^-46, median 2^-44.8): either side of the

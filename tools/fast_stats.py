@@ -24,10 +24,11 @@ for k in (1, 2, 3, 4):
     g = K.generate(c, 0, c.count)
     torch.cuda.synchronize()
     fn(buf, 1)
+    d0 = lib.kog_svd2_deferred_count()
     K.svd2(g)
     torch.cuda.synchronize()
     fn(buf, 1)
-    d = lib.kog_svd2_deferred_count()
+    d = lib.kog_svd2_deferred_count() - d0
     print(f"cfg{k}: deferred {d / c.count:.4f}; events per matrix:",
           {NAMES[i]: round(buf[i] / c.count, 4) for i in range(32) if buf[i]})
     print("   div sites (zero numerator):", {i: round(buf[32 + i] / c.count, 4) for i in range(32) if buf[32 + i]})
