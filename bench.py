@@ -32,7 +32,13 @@ sys.path.insert(0, ROOT)
 METRIC = "2x2 SVDs/sec (fp64 general)"
 UNIT = "matrices/s"
 HBM_FALLBACK = 6650.0
-REF_OPS_CFG3 = 203  # reference-sequence FP64 ops per cfg3 matrix (measured by op-count shim)
+# Reference-sequence FP64 ops per matrix (counted on the
+# reference's own operation sequence by the op-counting shim, Appendix A): the
+# decomposition (svd2) per config and the study (svd2 + svd2_ext + metrics).
+# cfg4's count is its binary64 ops (the binary32 ones, 62, run on the FP32 pipe).
+W_SVD2 = {1: 1787, 2: 88, 3: 203, 4: 328}
+W_STUDY = {1: 4546, 2: 1279, 3: 1907, 4: 2803}
+REF_OPS_CFG3 = W_SVD2[3]
 
 
 def peaks() -> dict:
@@ -108,6 +114,40 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def roofline(rate: float, bpm: int, w_ops: int, pk: dict, fp64_ops_s: float | None, kernel_s: float,
+             traffic_bpm: float | None, kernel: str, n: int) -> dict:
+    """Both bounds of one decomposition kernel: HBM (algorithmic bytes per
+    matrix x rate vs the measured copy bandwidth) and FP64 (the reference's op
+    count W per matrix x rate vs the in-run DFMA probe, one op per FMA); the
+    binding one is the lower matrices/s."""
+    achieved = bpm * rate / 1e9
+    hbm_rate = pk["hbm_gbs"] * 1e9 / bpm
+    out = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+           "frac": achieved / pk["hbm_gbs"], "traffic": None if traffic_bpm is None else traffic_bpm * n,
+           "traffic_bytes_per_matrix": traffic_bpm, "algorithmic_bytes_per_launch": bpm * n,
+           "peak_source": pk["source"], "kernel": kernel, "bytes_per_matrix": bpm, "kernel_ms": kernel_s * 1e3,
+           "hbm_bound_rate": hbm_rate}
+    if fp64_ops_s:
+        fp_rate = fp64_ops_s / w_ops
+        out.update({"fp64_ops_per_matrix": w_ops, "fp64_peak_tops": fp64_ops_s / 1e12, "fp64_bound_rate": fp_rate,
+                    "fp64_achieved_tops": w_ops * rate / 1e12, "frac_fp64": rate / fp_rate,
+                    "frac_hbm": achieved / pk["hbm_gbs"]})
+        out["binding"] = "hbm" if hbm_rate <= fp_rate else "fp64"
+        out["frac_binding"] = rate / min(hbm_rate, fp_rate)
+    return out
+
+
 # -------------------------------------------------------- reference arm
 def run_reference(args) -> None:
     """The reference's own CPU implementation (oracle/_ref: the unmodified
@@ -151,7 +191,7 @@ def run_reference(args) -> None:
         "data": "synthetic (seeded counter-based generator, SURVEY.md §8d)",
         "config": {"workload": f"cfg{args.config} sample of {cfg.count} matrices, reference svd2 on {threads} host threads",
                    "model": "enhanced 2x2 Kogbetliantz svd2", "global_batch": cfg.count, "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "cpu_model": cpu_model(),
                          "sample": f"{cfg.count} cfg{args.config} matrices per step, std::thread over 4096-blocks"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -186,7 +226,8 @@ def cpu_baseline(g_host, single: bool) -> dict:
     rate = n / dt
     n2 = int(min(g_host.shape[1], max(n, rate * 8.0)))
     dt2 = run(n2)
-    return {"value": n2 / dt2, "unit": UNIT, "cores": threads, "kind": "reference",
+    return {"value": n2 / dt2, "unit": UNIT, "cores": threads, "kind": "reference", "cpu_model": cpu_model(),
+            "nproc": os.cpu_count(), "flags": "g++ -std=c++20 -O3 -DNDEBUG -ffp-contract=off (proj/CMakeLists.txt Release)",
             "sample": f"first {n2} matrices of the same workload, reference svd2 (oracle/_ref), "
                       f"std::thread over 4096-blocks, {dt2:.1f} s"}
 
@@ -219,6 +260,7 @@ def study_cpu_baseline(K) -> dict | None:
     dt, row = run(n)
     gpu = K.csv_row(configs.cfg(5, count=n), K.run_batch(configs.cfg(5, count=n)))
     return {"value": n / dt, "unit": UNIT, "cores": int(ref.hardware_threads()), "kind": "reference",
+            "cpu_model": cpu_model(),
             "sample": f"first {n} config-5 matrices, reference run_batch (oracle/_ref, threads=0), {dt:.1f} s",
             "csv_equal": gpu == row}
 
@@ -226,7 +268,8 @@ def study_cpu_baseline(K) -> dict | None:
 def fp64_probe(K, torch) -> dict:
     """Achievable FP64 FMA rate on this GPU (DFMA chains, 8 per thread)."""
     lib = K._lib()
-    threads = 148 * 2048 * 4
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    threads = sms * 2048 * 4
     iters = 4096
     sink = torch.empty(threads, dtype=torch.float64, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
@@ -239,7 +282,43 @@ def fp64_probe(K, torch) -> dict:
     torch.cuda.synchronize()
     s = e0.elapsed_time(e1) / 1e3
     flops = threads * iters * 8 * 2
-    return {"dfma_tflops": flops / s / 1e12, "how": f"{threads} threads x {iters} x 8 independent DFMA chains"}
+    return {"dfma_tflops": flops / s / 1e12, "fma_ops_per_s": flops / 2 / s, "sms": sms,
+            "how": f"{threads} threads x {iters} x 8 independent DFMA chains"}
+
+
+def time_svd2(K, torch, g, out, steps: int, warmup: int, local: int, flush=None):
+    """K timed kog_svd2_batch calls over resident inputs, CUDA events on the
+    launching stream around each call; with `flush` (a buffer larger than L2)
+    the L2 is overwritten between calls, outside the timed events."""
+    for _ in range(warmup):
+        K.svd2(g, out=out)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    launches0 = K.launch_count()
+    with ClockSampler(local) as clk:
+        for e0, e1 in ev:
+            if flush is not None:
+                flush.add_(1)
+            e0.record()
+            K.svd2(g, out=out)
+            e1.record()
+        torch.cuda.synchronize()
+    launches = K.launch_count() - launches0
+    per = [e0.elapsed_time(e1) / 1e3 for e0, e1 in ev]
+    span = ev[0][0].elapsed_time(ev[-1][1]) / 1e3
+    return {"per": per, "span": span, "kernel_s": sum(per) / len(per), "launches": launches, "clocks": clk.summary()}
+
+
+def load_traffic() -> dict:
+    """ncu DRAM bytes per matrix of one kog_svd2_batch call per config
+    (profiles/svd2_traffic.json, captured by tools/measure_traffic.sh on the
+    current kernels)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "svd2_traffic.json")) as f:
+            tr = json.load(f)
+        return {int(k): v for k, v in tr.get("dram_bytes_per_matrix", {}).items()}
+    except Exception:
+        return {}
 
 
 def l2_note(nbytes: int) -> str:
@@ -267,6 +346,7 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-study", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg1/cfg2/cfg4 sub-records")
     ap.add_argument("--study-count", type=int, default=1 << 31, help="config-5 matrices over all ranks")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -315,36 +395,54 @@ def main() -> None:
     torch.cuda.synchronize()
 
     # ---- hot path: K launches of svd2 over resident inputs (inputs > L2)
-    for _ in range(args.warmup):
-        K.svd2(g, out=out)
-    torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches0 = K.launch_count()
-    with ClockSampler(local) as clk:
-        for e0, e1 in ev:
-            e0.record()
-            K.svd2(g, out=out)
-            e1.record()
-        torch.cuda.synchronize()
-    launches = K.launch_count() - launches0
+    tm = time_svd2(K, torch, g, out, args.steps, args.warmup, local)
+    launches, clocks = tm["launches"], tm["clocks"]
     barrier()
-    per = [e0.elapsed_time(e1) / 1e3 for e0, e1 in ev]
-    total_s = ev[0][0].elapsed_time(ev[-1][1]) / 1e3
-    total_s = max_over_ranks(total_s)
-    kern_s = sum(per) / len(per)
+    total_s = max_over_ranks(tm["span"])
+    kern_s = tm["kernel_s"]
     value = world * n * args.steps / total_s
     pk = peaks()
-    achieved = bpm * n / kern_s / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "svd2_traffic.json")) as f:
-            tr = json.load(f)
-        if tr.get("config") == args.config:
-            traffic = tr["dram_bytes_per_matrix"] * n
-    except Exception:
-        pass
+    traffic = load_traffic()
+    fp64 = fp64_probe(K, torch)
+    fp64_ops = fp64["fma_ops_per_s"]
+    main_roof = roofline(n / kern_s, bpm, W_SVD2[args.config], pk, fp64_ops, kern_s, traffic.get(args.config),
+                         f"k_svd2_fast + k_svd2_list (one kog_svd2_batch_{suf} call)", n)
+
+    # ---- the other BASELINE configs' decompositions (parity-test sizes of their own; one GPU each)
+    per_config = {}
+    if not args.no_configs and rank == 0 and world == 1:
+        del_main = False
+        for k in (1, 2, 4):
+            if k == args.config:
+                continue
+            if not del_main:
+                del g, out
+                torch.cuda.empty_cache()
+                del_main = True
+            ck = configs.cfg(k)
+            nk = configs.FULL_SIZE[k]
+            sk = "f32" if ck.single_precision else "f64"
+            gk = K.generate(ck, 0, nk, dev)
+            ok = K.empty_result(nk, gk.dtype, dev)
+            bk = configs.BYTES_PER_MATRIX[sk]
+            flush = torch.empty(64 << 20, dtype=torch.int64, device=dev) if nk * bk < 4 * 126 * 2**20 else None
+            tk = time_svd2(K, torch, gk, ok, max(args.steps, 10), args.warmup, local, flush)
+            rk = nk / tk["kernel_s"]
+            per_config[f"cfg{k}"] = {
+                "workload": f"cfg{k}: {nk} {SHAPE_OF[k]} {sk} 2x2 matrices", "value": rk, "unit": UNIT,
+                "ms_per_step": tk["kernel_s"] * 1e3, "steps": max(args.steps, 10), "dtype": sk,
+                "l2": l2_note(nk * bk) + ("; L2 overwritten (512 MiB write) before every timed call, outside "
+                                          "the timed events" if flush is not None else ""),
+                "roofline": roofline(rk, bk, W_SVD2[k], pk, fp64_ops, tk["kernel_s"], traffic.get(k),
+                                     f"k_svd2_fast + k_svd2_list (one kog_svd2_batch_{sk} call)", nk),
+                "clocks": tk["clocks"], "gpu_launches": tk["launches"]}
+            del gk, ok, flush
+            torch.cuda.empty_cache()
+        if del_main:  # the main config's buffers back for the e2e leg below
+            g = K.generate(base, lo, n, dev)
+            out = K.empty_result(n, g.dtype, dev)
 
     # ---- fused study over config 5 with the NCCL stats all-reduce
     study = None
@@ -352,12 +450,17 @@ def main() -> None:
         cfg5 = configs.cfg(5, count=args.study_count)
         slo, shi = kdist.shard(cfg5.count, rank, world)
         ss = K.StudyStats()
+        # N>1: the stats slots all-reduced by the library's C++ side on its own NCCL
+        # communicator (kog_study_allreduce); gloo runs (functional checks) use torch's
+        nccl = kdist.NcclStats() if world > 1 and os.environ.get("KOG2_BENCH_BACKEND", "nccl") == "nccl" else None
 
         def study_step():
             ss.reset()
             ss.add(cfg5, slo, shi - slo)
             st = ss.read()
-            return kdist.allreduce_stats(st, device=dev) if world > 1 else st
+            if world == 1:
+                return st
+            return nccl.allreduce(st) if nccl is not None else kdist.allreduce_stats(st)
 
         study_step()
         barrier()
@@ -366,10 +469,22 @@ def main() -> None:
         st = study_step()
         torch.cuda.synchronize()
         dt = max_over_ranks(time.perf_counter() - t0)
+        srate = cfg5.count / dt
+        sbound = fp64_ops / W_STUDY[3]
         study = {"metric": "fused study matrices/s (generate+svd2+svd2_ext+metrics+reduce)",
-                 "value": cfg5.count / dt, "unit": UNIT, "count": cfg5.count, "seconds": dt,
-                 "scaling": "strong", "csv": K.csv_row(cfg5, st)}
+                 "value": srate, "unit": UNIT, "count": cfg5.count, "seconds": dt,
+                 "scaling": "strong", "csv": K.csv_row(cfg5, st),
+                 "allreduce": ("kog_study_allreduce (C++ ncclAllReduce MAX of the packed stats)" if nccl is not None
+                               else ("torch.distributed all_reduce of the packed stats" if world > 1 else None)),
+                 "roofline": {"bound": "fp64", "unit": "TOP/s", "ops_per_matrix": W_STUDY[3],
+                              "achieved": W_STUDY[3] * srate / 1e12, "peak": fp64_ops / 1e12,
+                              "frac": srate / sbound, "bound_rate": sbound,
+                              "note": "reference-sequence FP64 ops (svd2 + svd2_ext + metrics, SURVEY.md §8(d)) "
+                                      "against the in-run DFMA probe, one op per FMA; HBM is not binding "
+                                      "(generated on device, ~200 B/matrix of chunk buffers)"}}
         ss.free()
+        if nccl is not None:
+            nccl.close()
 
     # ---- end to end through the public host-buffer API (pinned host memory)
     e2e = None
@@ -401,7 +516,6 @@ def main() -> None:
         cpu = cpu_baseline(g_host, base.single_precision)
         if study is not None:
             study["cpu_baseline"] = study_cpu_baseline(K)
-    fp64 = fp64_probe(K, torch) if rank == 0 else None
 
     if rank == 0:
         line = {
@@ -414,15 +528,11 @@ def main() -> None:
                        "model": "enhanced 2x2 Kogbetliantz svd2 (arXiv 2407.13116)", "global_batch": world * n,
                        "parallelism": f"dp{world} (index-range shards, no data-path collective)",
                        "l2": l2_note(n * bpm)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk["source"],
-                         "kernel": "k_svd2_fast + k_svd2_list (one kog_svd2_batch_f64 call)", "bytes_per_matrix": bpm, "kernel_ms": kern_s * 1e3},
-            "e2e": e2e, "cpu_baseline": cpu, "study": study, "gpu_launches": launches,
-            "clocks": clk.summary(), "fp64": fp64,
+            "roofline": main_roof,
+            "e2e": e2e, "cpu_baseline": cpu, "study": study, "configs": per_config or None,
+            "gpu_launches": launches, "clocks": clocks, "fp64": fp64,
             "bit_exact": "outputs bit-identical to the reference (tests/test_gpu_parity.py)",
         }
-        if fp64 and args.config == 3:
-            fp64["ref_equiv_tops"] = REF_OPS_CFG3 * n / kern_s / 1e12
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

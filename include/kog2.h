@@ -375,6 +375,35 @@ int kog_run_batch(const kog_run_config* cfg, kog_stats* out);
 /* BatchAbort text for a failure key (harness.hpp:194-198). */
 int kog_abort_message(const kog_run_config* cfg, uint64_t fail_key, char* buf, size_t cap);
 
+/* --------------------------------------------------------- multi-GPU study */
+/* contiguous index shards [k*N/G, (k+1)*N/G) (the last takes
+ * the remainder), one study per device, and ONE ncclAllReduce(MAX) of a small
+ * packed int64 vector; the per-rank blocks are merged on the host in rank
+ * order (ErrorStats::merge, harness.hpp:96-105), so any device count gives the
+ * stats (and CSV row) of kog_run_batch.  NCCL is dlopen'ed on first use
+ * (libnccl.so.2); KOG_ERR_NODEV if it is absent. */
+void kog_study_shard(uint64_t count, int rank, int world, uint64_t* lo, uint64_t* hi);
+size_t kog_stats_slot_count(int world);
+/* slots[kog_stats_slot_count(world)]: 0-4 metric bit patterns, 5 kappa_inf,
+ * 6 = 2^62 - fail_key (or -1), then 23 fields per rank as 32-bit halves */
+int kog_stats_pack(const kog_stats* st, int rank, int world, int64_t* slots);
+int kog_stats_unpack(const int64_t* slots, int world, kog_stats* out);
+/* One process per device (torchrun / MPI): rank 0 makes the id, the caller
+ * distributes its 128 bytes, every rank makes its communicator on its current
+ * device, and kog_study_allreduce combines that rank's host stats in place. */
+int kog_nccl_available(void);
+int kog_nccl_unique_id(uint8_t* id, size_t cap);
+int kog_nccl_comm_init(const uint8_t* id, int world, int rank, void** comm);
+int kog_nccl_comm_destroy(void* comm);
+int kog_study_allreduce(void* comm, int rank, int world, kog_stats* stats, void* stream);
+/* One process, one host thread per device (the reference's run_batch worker
+ * pool, harness.hpp:226-271, with devices as workers): the whole study of cfg
+ * over devices[0..ndev) (NULL = 0..ndev-1), synchronous.  *device_seconds
+ * (optional) = max over devices of the device time of study + all-reduce.
+ * Returns KOG_ERR_ABORT with the BatchAbort text like kog_run_batch. */
+int kog_study_multi(const kog_run_config* cfg, const int* devices, int ndev, kog_stats* out,
+                    double* device_seconds);
+
 /* csv_header / csv_row (harness.hpp:286-317); returns the length written. */
 int kog_csv_header(char* buf, size_t cap);
 int kog_csv_row(const kog_run_config* cfg, const kog_stats* st, char* buf, size_t cap);

@@ -241,14 +241,15 @@ ErrorStats stats_from_c(const kog_stats* o) {
 // run_one/run_batch for the extended regime: the reference's own per-matrix
 // body (harness.hpp:190-222) over the extended generator.
 template <class T>
-ErrorStats run_ext(const kog_run_config* c, std::string& fail) {
+ErrorStats run_ext(const kog_run_config* c, std::string& fail, uint64_t index0 = 0, uint64_t count = UINT64_MAX) {
   const RunConfig cfg = to_rc(c);
+  const uint64_t n = count == UINT64_MAX ? c->count : count;
   constexpr uint64_t kBlock = 4096;
-  const uint64_t nblocks = (c->count + kBlock - 1) / kBlock;
+  const uint64_t nblocks = (n + kBlock - 1) / kBlock;
   std::vector<ErrorStats> bs(nblocks);
   std::vector<std::string> bf(nblocks);
-  parallel_blocks(c->count, c->threads, [&](uint64_t b, uint64_t lo, uint64_t hi) {
-    for (uint64_t i = lo; i < hi; ++i) {
+  parallel_blocks(n, c->threads, [&](uint64_t b, uint64_t lo, uint64_t hi) {
+    for (uint64_t i = index0 + lo; i < index0 + hi; ++i) {
       const Matrix2<T> g = gen_any<T>(c, i);
       const ExtSvd ref = svd2_ext(g);
       auto failmsg = [&](const char* what) {
@@ -668,6 +669,19 @@ int kogref_run_batch(const kog_run_config* c, kog_stats* out) {
     g_err = e.what();
     return -1;
   }
+}
+
+// the reference's run_one body over indices [index0, index0 + n) in 4096-blocks
+// merged in order (harness.hpp:190-271 on a sub-range): one shard of a study
+int kogref_run_range(const kog_run_config* c, uint64_t index0, uint64_t n, kog_stats* out) {
+  std::string fail;
+  const ErrorStats st = c->single_precision ? run_ext<float>(c, fail, index0, n) : run_ext<double>(c, fail, index0, n);
+  if (!fail.empty()) {
+    g_err = fail;
+    return -4;
+  }
+  stats_to_c(st, out);
+  return 0;
 }
 
 int kogref_csv_row(const kog_run_config* c, const kog_stats* st, char* buf, size_t cap) {

@@ -57,6 +57,7 @@ _COMMON = {
     "generate_f64": (i32, [PTR(capi.kog_run_config), u64, PTR(capi.kog_mat), u64, i32]),
     "generate_f32": (i32, [PTR(capi.kog_run_config), u64, PTR(capi.kog_mat), u64, i32]),
     "run_batch": (i32, [PTR(capi.kog_run_config), PTR(capi.kog_stats)]),
+    "run_range": (i32, [PTR(capi.kog_run_config), u64, u64, PTR(capi.kog_stats)]),
     "csv_row": (i32, [PTR(capi.kog_run_config), PTR(capi.kog_stats), C.c_char_p, C.c_size_t]),
     "lasv2_f64": (i32, [P, P, P, P, u64]),
     "lasv2_f32": (i32, [P, P, P, P, u64]),
@@ -147,6 +148,13 @@ def records(ctype, n: int):
 def run_batch(lib: Lib, cfg: capi.kog_run_config):
     st = capi.kog_stats()
     rc = lib.run_batch(C.byref(cfg), C.byref(st))
+    return rc, st, lib.last_error().decode()
+
+
+def run_range(lib: Lib, cfg: capi.kog_run_config, index0: int, n: int):
+    """The reference's run_one over indices [index0, index0 + n): one shard."""
+    st = capi.kog_stats()
+    rc = lib.run_range(C.byref(cfg), index0, n, C.byref(st))
     return rc, st, lib.last_error().decode()
 
 

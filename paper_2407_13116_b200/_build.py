@@ -35,7 +35,7 @@ CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math"
              f"-I{CUDA_HOME}/include", f"-I{ROOT}/include"]
 
 CU_SOURCES = ["kog2_k_svd2.cu", "kog2_k_units.cu", "kog2_k_study.cu"]
-CXX_SOURCES = ["kog2_host.cpp", "kog2_ws.cpp"]
+CXX_SOURCES = ["kog2_host.cpp", "kog2_ws.cpp", "kog2_multi.cpp"]
 HEADERS = [f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] if os.path.isdir(CSRC) else []
 
 
@@ -83,7 +83,7 @@ def build(force: bool = False, verbose: bool = False, variant: str | None = None
     with ThreadPoolExecutor(max_workers=4) as ex:
         list(ex.map(lambda j: _run(*j), jobs))
     if force or jobs or _newer(lib, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lpthread"])
+        _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lpthread", "-ldl"])
     if not variant:  # the svd2batch-compatible CLI, linked against the library (no CUDA runtime of its own)
         os.makedirs(BINDIR, exist_ok=True)
         cli_src = os.path.join(CSRC, "svd2batch.cpp")

@@ -182,6 +182,26 @@ PROTOTYPES: dict[str, tuple] = {
     "kog_div_batch_f64": (i32, [P, P, P, u64, P]),
     "kog_div_batch_f32": (i32, [P, P, P, u64, P]),
     "kog_launch_count": (C.c_uint64, []),
+    # host-buffer forms (the C++ shim's surface)
+    "kog_hypot_host_f64": (i32, [P, P, P, u64]),
+    "kog_hypot_host_f32": (i32, [P, P, P, u64]),
+    "kog_svd2_ext_host_f64": (i32, [PTR(kog_mat), P, u64]),
+    "kog_svd2_ext_host_f32": (i32, [PTR(kog_mat), P, u64]),
+    "kog_metrics_host_f64": (i32, [PTR(kog_mat), P, u64, PTR(kog_options)]),
+    "kog_metrics_host_f32": (i32, [PTR(kog_mat), P, u64, PTR(kog_options)]),
+    "kog_generate_host_f64": (i32, [PTR(kog_run_config), u64, PTR(kog_mat), u64]),
+    "kog_generate_host_f32": (i32, [PTR(kog_run_config), u64, PTR(kog_mat), u64]),
+    # multi-GPU study
+    "kog_study_shard": (None, [u64, i32, i32, PTR(u64), PTR(u64)]),
+    "kog_stats_slot_count": (C.c_size_t, [i32]),
+    "kog_stats_pack": (i32, [PTR(kog_stats), i32, i32, P]),
+    "kog_stats_unpack": (i32, [P, i32, PTR(kog_stats)]),
+    "kog_nccl_available": (i32, []),
+    "kog_nccl_unique_id": (i32, [P, C.c_size_t]),
+    "kog_nccl_comm_init": (i32, [P, i32, i32, PTR(P)]),
+    "kog_nccl_comm_destroy": (i32, [P]),
+    "kog_study_allreduce": (i32, [P, i32, i32, PTR(kog_stats), P]),
+    "kog_study_multi": (i32, [PTR(kog_run_config), P, i32, PTR(kog_stats), PTR(C.c_double)]),
 }
 
 _lib = None

@@ -4,8 +4,9 @@
 // current CUDA device through the C-ABI (kog_run_batch, kog_csv_row).
 //
 // Extensions: --regime ranged with --elo/--ehi, --tail LO..HI:MOD and
-// --zero-mask (the BASELINE config generator rules, include/kog2.h), and
-// --device N.
+// --zero-mask (the BASELINE config generator rules, include/kog2.h),
+// --device N, and --gpus N (the study sharded over devices 0..N-1 with one
+// NCCL all-reduce of the stats, kog_study_multi; the CSV is the same).
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -23,7 +24,7 @@ int usage(const char* msg) {
             << "usage: kog2_svd2batch [--precision single|double] [--shape tri|gen] [--regime circ|bullet|sigma|ranged]\n"
                "                      [--varsigma N] [--count N] [--seed HEX] [--routine kog|lasv2] [--threads N]\n"
                "                      [--out PATH] [--sweep varsigma=A..B:step] [--emulate-noncr-hypot]\n"
-               "                      [--elo E --ehi E] [--tail LO..HI:MOD] [--zero-mask] [--device N]\n";
+               "                      [--elo E --ehi E] [--tail LO..HI:MOD] [--zero-mask] [--device N] [--gpus N]\n";
   return 2;
 }
 
@@ -43,7 +44,7 @@ int main(int argc, char** argv) {
   cfg.count = 1ull << 20;
   cfg.threads = 1;
   cfg.options.hypot_is_cr = 1;
-  int device = -1;
+  int device = -1, gpus = 0;
   for (int i = 1; i < argc; ++i) {
     const std::string a = argv[i];
     auto need = [&](const char* what) -> const char* {
@@ -70,7 +71,7 @@ int main(int argc, char** argv) {
       if (a == "--sweep") sweep_spec = s;
       if (a == "--tail") tail_spec = s;
     } else if (a == "--varsigma" || a == "--count" || a == "--threads" || a == "--elo" || a == "--ehi" ||
-               a == "--device") {
+               a == "--device" || a == "--gpus") {
       if (!(v = need(a.c_str())) || !parse_int(v, n)) return usage(("bad value for " + a).c_str());
       if (a == "--varsigma") cfg.varsigma = static_cast<int32_t>(n);
       if (a == "--count") {
@@ -81,6 +82,10 @@ int main(int argc, char** argv) {
       if (a == "--elo") cfg.elo = static_cast<int32_t>(n);
       if (a == "--ehi") cfg.ehi = static_cast<int32_t>(n);
       if (a == "--device") device = static_cast<int>(n);
+      if (a == "--gpus") {
+        if (n < 1) return usage("--gpus must be >= 1");
+        gpus = static_cast<int>(n);
+      }
     } else {
       return usage(("unknown argument " + a).c_str());
     }
@@ -114,6 +119,9 @@ int main(int argc, char** argv) {
     std::cerr << "bad --seed, expected hexadecimal\n";
     return 2;
   }
+  if (device >= 0 && gpus > 0) return usage("--device and --gpus are exclusive");
+  // NCCL's own log lines (NCCL_DEBUG) go to stdout unless redirected: keep the CSV clean
+  if (gpus > 0 && !std::getenv("NCCL_DEBUG_FILE")) setenv("NCCL_DEBUG_FILE", "/dev/stderr", 1);
   if (device >= 0 && kog_set_device(device) != KOG_OK) {
     std::cerr << "cannot select CUDA device " << device << "\n";
     return 2;
@@ -135,7 +143,7 @@ int main(int argc, char** argv) {
   *out << buf << "\n";
   auto run = [&]() -> int {
     kog_stats st;
-    const int rc = kog_run_batch(&cfg, &st);
+    const int rc = gpus > 0 ? kog_study_multi(&cfg, nullptr, gpus, &st, nullptr) : kog_run_batch(&cfg, &st);
     if (rc == KOG_ERR_ABORT) {
       std::cerr << "batch aborted: " << kog_last_error() << "\n";
       return 1;

@@ -18,77 +18,35 @@ The host merges the rank blocks in rank order with kog_stats_merge
 from __future__ import annotations
 
 import ctypes as C
-import struct
 
 import numpy as np
 
 from . import capi
 
-_FIELDS_PER_RANK = 4 + 19  # kappa e, hi, lo, index + 19 counters
-HEAD = 7
-NO_FAIL = -1
-FAIL_BASE = 1 << 62
-
 
 def shard(count: int, rank: int, world: int) -> tuple[int, int]:
-    """[lo, hi) of rank's contiguous index range (last shard takes the remainder)."""
-    per = count // world
-    lo = rank * per
-    hi = count if rank == world - 1 else lo + per
-    return lo, hi
-
-
-def _u64(x: float) -> int:
-    return struct.unpack("<Q", struct.pack("<d", x))[0]
-
-
-def _f64(u: int) -> float:
-    return struct.unpack("<d", struct.pack("<Q", u & 0xFFFFFFFFFFFFFFFF))[0]
-
-
-def _rank_fields(st: capi.kog_stats) -> list[int]:
-    f = [st.max_kappa2.e & 0xFFFFFFFFFFFFFFFF, _u64(st.max_kappa2.hi), _u64(st.max_kappa2.lo), st.max_kappa2_index]
-    f += list(st.t2p) + list(st.path)
-    f += [st.tanpsi_inf, st.diag_swap, st.compose_minus, st.sigma_swap, st.prescale_inexact]
-    return f
+    """[lo, hi) of rank's contiguous index range (last shard takes the
+    remainder): kog_study_shard."""
+    lo, hi = C.c_uint64(), C.c_uint64()
+    capi.load().kog_study_shard(count, rank, world, C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
 
 
 def pack(st: capi.kog_stats, rank: int, world: int) -> np.ndarray:
-    buf = np.zeros(HEAD + 2 * _FIELDS_PER_RANK * world, dtype=np.int64)
-    for k, name in enumerate(("reG", "reS1", "reS2", "reU", "reV")):
-        buf[k] = _u64(getattr(st, name))
-    buf[5] = 1 if st.kappa_inf else 0
-    buf[6] = NO_FAIL if st.fail_key == 0xFFFFFFFFFFFFFFFF else FAIL_BASE - st.fail_key
-    base = HEAD + 2 * _FIELDS_PER_RANK * rank
-    for k, v in enumerate(_rank_fields(st)):
-        buf[base + 2 * k] = v >> 32
-        buf[base + 2 * k + 1] = v & 0xFFFFFFFF
+    """kog_stats_pack: this rank's stats as the int64 slot vector."""
+    lib = capi.load()
+    buf = np.zeros(lib.kog_stats_slot_count(world), dtype=np.int64)
+    capi.check(lib.kog_stats_pack(C.byref(st), rank, world, buf.ctypes.data))
     return buf
 
 
 def unpack(buf: np.ndarray, world: int) -> capi.kog_stats:
-    lib = capi.load()
-    total = capi.kog_stats()
-    lib.kog_stats_init(C.byref(total))
-    for r in range(world):
-        base = HEAD + 2 * _FIELDS_PER_RANK * r
-        v = [(int(buf[base + 2 * k]) << 32) | int(buf[base + 2 * k + 1]) for k in range(_FIELDS_PER_RANK)]
-        part = capi.kog_stats()
-        lib.kog_stats_init(C.byref(part))
-        e = v[0] - (1 << 64) if v[0] >= (1 << 63) else v[0]
-        part.max_kappa2 = capi.kog_extfloat(e, _f64(v[1]), _f64(v[2]))
-        part.max_kappa2_index = v[3]
-        for k in range(7):
-            part.t2p[k] = v[4 + k]
-            part.path[k] = v[11 + k]
-        (part.tanpsi_inf, part.diag_swap, part.compose_minus, part.sigma_swap,
-         part.prescale_inexact) = v[18:23]
-        lib.kog_stats_merge(C.byref(total), C.byref(part))
-    for k, name in enumerate(("reG", "reS1", "reS2", "reU", "reV")):
-        setattr(total, name, _f64(int(buf[k])))
-    total.kappa_inf = int(buf[5])
-    total.fail_key = 0xFFFFFFFFFFFFFFFF if int(buf[6]) == NO_FAIL else FAIL_BASE - int(buf[6])
-    return total
+    """kog_stats_unpack: the MAX-reduced slot vector back into stats, the rank
+    blocks merged in rank order."""
+    buf = np.ascontiguousarray(buf, dtype=np.int64)
+    out = capi.kog_stats()
+    capi.check(capi.load().kog_stats_unpack(buf.ctypes.data, world, C.byref(out)))
+    return out
 
 
 def allreduce_stats(st: capi.kog_stats, group=None, device=None) -> capi.kog_stats:
@@ -104,3 +62,37 @@ def allreduce_stats(st: capi.kog_stats, group=None, device=None) -> capi.kog_sta
         t = t.to(device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return unpack(t.cpu().numpy(), world)
+
+
+class NcclStats:
+    """The NCCL all-reduce of the stats slots issued from the library's C++
+    side (kog_study_allreduce) on a communicator of its own: rank 0's unique id
+    travels through torch.distributed (plumbing only), every rank builds its
+    communicator on its current CUDA device."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+
+        lib = capi.load()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            capi.check(lib.kog_nccl_unique_id(uid, 128))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        C.memmove(uid, box[0], 128)
+        self.comm = C.c_void_p()
+        capi.check(lib.kog_nccl_comm_init(uid, self.world, self.rank, C.byref(self.comm)))
+        self._stream = torch.cuda.current_stream().cuda_stream
+
+    def allreduce(self, st: capi.kog_stats) -> capi.kog_stats:
+        out = capi.kog_stats.from_buffer_copy(bytes(st))
+        capi.check(capi.load().kog_study_allreduce(self.comm, self.rank, self.world, C.byref(out), self._stream))
+        return out
+
+    def close(self):
+        if self.comm:
+            capi.load().kog_nccl_comm_destroy(self.comm)
+            self.comm = C.c_void_p()

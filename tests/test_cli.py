@@ -64,3 +64,18 @@ def test_cli_lasv2_sweep_and_invalid(cuda, tmp_path):
     r = run("--shape", "gen", "--regime", "ranged", "--elo", "-500", "--ehi", "500", "--zero-mask", "--count", "4096",
             "--seed", "f1e2d3c")
     assert r.stdout.splitlines()[1].startswith("double,gen,ranged,0,4096,000000000f1e2d3c,kog,")
+
+
+@pytest.mark.gpu
+def test_cli_gpus_flag_matches_single_device(cuda, tmp_path):
+    """--gpus N runs the study through kog_study_multi (shards + one NCCL
+    all-reduce); on the box's devices the row equals the single-device one."""
+    import torch
+    n = torch.cuda.device_count()
+    base = ["--shape", "gen", "--regime", "ranged", "--elo", "-500", "--ehi", "500", "--zero-mask", "--count",
+            str(3 * (1 << 20) + 5), "--seed", "f1e2d3c"]
+    csv = lambda out: [ln for ln in out.splitlines() if ln.startswith(("precision,", "double,", "single,"))]
+    one = run(*base).stdout
+    multi = run(*base, "--gpus", str(n)).stdout  # (NCCL may add its own version line)
+    assert len(csv(one)) == 2 and csv(multi) == csv(one)
+    assert run(*base, "--gpus", "1", "--device", "0", check=False).returncode == 2

@@ -316,6 +316,10 @@ def test_hypot_adversarial_edges(cuda, ref, dt):
     sq = np.array([2.0, 1.0, 1.0, -np.inf, -np.inf], dtype=dt)
     g2 = host(K.hypot_cr(dev(sp), dev(sq)))
     assert np.isinf(g2[0]) and np.isinf(g2[1]) and np.isnan(g2[2]) and np.isinf(g2[3]) and np.isinf(g2[4])
+    # a NaN in either place next to every edge value (normal, subnormal, zero): NaN (a + b)
+    nan = np.full(e.size, np.nan, dtype=dt)
+    assert np.isnan(host(K.hypot_cr(dev(e), dev(nan)))).all()
+    assert np.isnan(host(K.hypot_cr(dev(nan), dev(e)))).all()
     assert float(host(K.hypot_cr(dev(np.array([nu], dt)), dev(np.array([1], dt))))[0]) == float(nu)
 
 
