@@ -17,6 +17,7 @@
 
 #include "kog2_common.cuh"
 #include "kog2_fast.cuh"
+#include "kog2_lean.cuh"
 
 using namespace kog2;
 
@@ -41,18 +42,26 @@ __device__ __forceinline__ uint32_t sign_flags(const Result<T>& r) {
   return f;
 }
 
-template <class T, class I>
+// STREAM: evict-first stores (whole sectors written once); the two-speed
+// kernel writes a sector's lanes at two moments and keeps the default policy
+// so that L2 merges them
+template <bool STREAM, class V>
+__device__ __forceinline__ void st_out(V* p, V v) {
+  if constexpr (STREAM) st_cs(p, v);
+  else *p = v;
+}
+template <bool STREAM = true, class T, class I>
 __device__ __forceinline__ void store_result(const OutP<T>& out, I i, const Result<T>& r) {
-  st_cs(out.sig1_f + i, r.sigma1.f);
-  st_cs(out.sig2_f + i, r.sigma2.f);
-  st_cs(out.sig1_e + i, static_cast<int32_t>(r.sigma1.e));
-  st_cs(out.sig2_e + i, static_cast<int32_t>(r.sigma2.e));
-  st_cs(out.u11 + i, r.u.g11);
-  st_cs(out.u12 + i, r.u.g12);
-  st_cs(out.v11 + i, r.v.g11);
-  st_cs(out.v12 + i, r.v.g12);
-  st_cs(out.s + i, static_cast<int32_t>(r.s));
-  st_cs(out.flags + i, r.flags | sign_flags(r));
+  st_out<STREAM>(out.sig1_f + i, r.sigma1.f);
+  st_out<STREAM>(out.sig2_f + i, r.sigma2.f);
+  st_out<STREAM>(out.sig1_e + i, static_cast<int32_t>(r.sigma1.e));
+  st_out<STREAM>(out.sig2_e + i, static_cast<int32_t>(r.sigma2.e));
+  st_out<STREAM>(out.u11 + i, r.u.g11);
+  st_out<STREAM>(out.u12 + i, r.u.g12);
+  st_out<STREAM>(out.v11 + i, r.v.g11);
+  st_out<STREAM>(out.v12 + i, r.v.g12);
+  st_out<STREAM>(out.s + i, static_cast<int32_t>(r.s));
+  st_out<STREAM>(out.flags + i, r.flags | sign_flags(r));
 }
 
 // the general algorithm over the whole batch
@@ -94,7 +103,8 @@ struct FastShape<float> {
 };
 template <class T>
 __global__ void __launch_bounds__(FastShape<T>::threads, FastShape<T>::minb)
-    k_svd2_fast(InP<T> in, OutP<T> out, uint64_t n, uint32_t* list, unsigned* count) {
+    k_svd2_fast(InP<T> in, OutP<T> out, uint64_t n, uint32_t* list, unsigned* count, const unsigned* gate) {
+  if (gate && *gate == 0u) return;  // k_svd2_lean kept the batch
   const unsigned lane = threadIdx.x & 31u;
   // 32-bit indices: n <= kFastChunk = 2^31 per launch, so i + stride < 2^32
   // (one 32x32->64 multiply-add per array address instead of 64-bit arithmetic)
@@ -117,6 +127,335 @@ __global__ void __launch_bounds__(FastShape<T>::threads, FastShape<T>::minb)
   }
 }
 
+// One matrix through the specialised path (k_svd2_fast's loop body): result
+// stored, a deferred lane appended to the list for k_svd2_list.
+template <class T, int CLS>
+__device__ __forceinline__ void fast_one(const InP<T>& in, const OutP<T>& out, unsigned i, uint32_t* list,
+                                         unsigned* count, unsigned lane) {
+  const Mat<T> g{in.g11[i], in.g12[i], in.g21[i], in.g22[i]};  // read a moment ago by the lean pass: L2
+  Result<T> r;
+  bool bad = false;
+  fast::svd2_fast<T, CLS>(g, r, bad);
+  store_result<false>(out, i, r);
+  const unsigned active = __activemask();
+  const unsigned m = __ballot_sync(active, bad);
+  if (m) {
+    const int leader = __ffs(m) - 1;
+    unsigned base = 0;
+    if (static_cast<int>(lane) == leader) base = atomicAdd(count, static_cast<unsigned>(__popc(m)));
+    base = __shfl_sync(active, base, leader);
+    if (bad) list[base + __popc(m & ((1u << lane) - 1u))] = i;
+  }
+}
+
+// binary64, default Options, large batches: the two-speed kernel.
+//
+// Each warp walks 32-matrix tiles through svd2_lean (kog2_lean.cuh: the
+// separated t' = 15 case, about a third of svd2_fast's instructions) and
+// sorts the lanes it does not cover into three queues in the block's shared
+// memory, by zero pattern, so that the rest of the work runs as full warps on
+// one route each:
+//   class 2  t = 15 and the one-row/column patterns that ride along urv15,
+//   class 0  svd_simple patterns: the warp whose push takes the queue across a
+//            multiple of 32 runs svd2_fast<2> (svd2_fast<0>) over those 32;
+//   class 1  t ~ 13: run by the whole block at once whenever 512 are queued
+//            (phase1: every warp takes 32), because its code is a quarter of
+//            the kernel's and the SM's instruction cache holds 32 KB — with
+//            every warp running every class whenever its push completed a
+//            batch, the kernel spent a quarter of its time waiting for
+//            instructions (profiles/r3_icache.txt); this way the other
+//            classes' 38 KB stay resident between phases.
+// The block's sixteen warps fill a batch of classes 2 and 0 within a tile or
+// two, so the queued matrices' inputs and the output sectors they share with
+// their neighbours are still in L2 when the batch runs.  Queue slots are
+// exact-turn words (q_put / q_take above); no block waits for another, and
+// tiles are handed out dynamically, eight consecutive tiles per grab.
+// Outputs: a sector must be written whole the first time (a first partial
+// write costs a DRAM fill read and a second write-back), so the lanes that are
+// queued store their (meaningless) lean result too and their batch overwrites
+// it a moment later; the fences order the two stores.  The next tile's inputs
+// are copied to shared memory while the current one is computed (cp.async).
+// A batch whose 512-matrix sample says svd2_lean would fail on more than about
+// half the matrices sets LeanGlobal::mode and leaves the whole batch to
+// k_svd2_fast, launched behind it.
+#ifndef KOG2_LEAN_PROBE
+#define KOG2_LEAN_PROBE 16
+#endif
+__device__ __forceinline__ unsigned ld_vol(const unsigned* p) { return *reinterpret_cast<const volatile unsigned*>(p); }
+#ifdef KOG2_LEAN_DEBUG
+// debug builds: spins are counted per site (in pinned host memory when set, so a hung kernel can be watched)
+__device__ unsigned g_lean_dbg[64];
+__device__ unsigned* g_lean_host = nullptr;
+#define KOG2_SPIN(cond, site, a, b)                                      \
+  do {                                                                   \
+    unsigned spins_ = 0;                                                 \
+    while (cond) {                                                       \
+      if ((++spins_ & 0xfffu) == 0u) {                                   \
+        atomicAdd(&g_lean_dbg[2 + (site)], 1u);                          \
+        if (g_lean_host) {                                               \
+          atomicAdd(&g_lean_host[(site)], 1u);                           \
+          if ((spins_ >> 12) == 64u) {                                   \
+            const unsigned k_ = 16u + 6u * (site);                       \
+            g_lean_host[k_] = blockIdx.x;                                \
+            g_lean_host[k_ + 1] = threadIdx.x;                           \
+            g_lean_host[k_ + 2] = (a);                                   \
+            g_lean_host[k_ + 3] = (b);                                   \
+          }                                                              \
+        }                                                                \
+      }                                                                  \
+    }                                                                    \
+  } while (0)
+#else
+#define KOG2_SPIN(cond, site, a, b) \
+  while (cond) {                    \
+  }
+#endif
+typedef unsigned long long u64;
+// Ring slots (multi-producer, multi-consumer, exact turns).  A slot word is
+// (state << 32) | index: state 2L = empty, lap L's producer may write; 2L + 1 =
+// holds lap L's index; the lap of position p in a ring of 2^k slots is p >> k.
+// The producer's wait and write are ONE compare-and-swap: with the store behind
+// a wait loop, a lane whose turn has come would sit at the loop's reconvergence
+// point until the warp's other lanes leave it — and a lane of another class may
+// be waiting for a batch that the warp waiting for THIS entry has yet to run.
+// Exact turns matter for the same reason: if a later lap's producer could take a
+// freed slot first, the earlier one would wait for a consumer that may in turn
+// be waiting for it (seen as a hang with free-for-all slots).  With both, every
+// wait is for a running warp's step on a strictly earlier reservation, so the
+// waits cannot form a cycle.
+__device__ __forceinline__ u64 q_word(unsigned state, unsigned v) { return (static_cast<u64>(state) << 32) | v; }
+__device__ __forceinline__ void q_put(u64* slot, unsigned lap, unsigned v, unsigned site) {
+  const u64 want = q_word(2u * lap, 0u);
+  KOG2_SPIN(atomicCAS(slot, want, q_word(2u * lap + 1u, v)) != want, site, lap, v);
+}
+__device__ __forceinline__ unsigned q_take(u64* slot, unsigned lap, unsigned site) {
+  volatile u64* vs = slot;
+  u64 w;
+  KOG2_SPIN(static_cast<unsigned>((w = *vs) >> 32) != 2u * lap + 1u, site, lap, 0u);
+  *vs = q_word(2u * lap + 2u, 0u);
+  return static_cast<unsigned>(w);
+}
+constexpr unsigned kLeanWarps = KOG2_FAST_THREADS / 32;
+constexpr unsigned kRing2 = 512;    // class 2 ring, a power of two
+constexpr unsigned kRing0 = 256;    // class 0 ring
+constexpr unsigned kRing1 = 2048;   // class 1 store (plain words: filled between phases, emptied inside them)
+constexpr unsigned kPhase1 = 32 * kLeanWarps;  // class 1 entries per phase
+constexpr unsigned kLeanChunk = 8;  // consecutive tiles per grab
+struct LeanGlobal {
+  unsigned next_chunk;
+  unsigned mode;  // 1: the batch goes to k_svd2_fast
+};
+struct LeanShared {
+  u64 slot2[kRing2];
+  u64 slot0[kRing0];
+  unsigned slot1[kRing1];
+  unsigned tail[3];   // reserved positions per class (free-running)
+  unsigned head1;     // class 1 positions already run (changes inside phases only)
+  unsigned phase;     // != 0: class 1 entries the block is to run now
+  unsigned done;      // warps out of tiles
+  unsigned finished;  // the block's last warp has run the remainders
+};
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void lean_fetch(double (*st)[32], const InP<double>& in, unsigned i, unsigned n32,
+                                           unsigned lane) {
+  if (i < n32) {
+    cp_async8(&st[0][lane], in.g11 + i);
+    cp_async8(&st[1][lane], in.g12 + i);
+    cp_async8(&st[2][lane], in.g21 + i);
+    cp_async8(&st[3][lane], in.g22 + i);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+// run the queued indices [pos, pos + cnt) of the class 2 or class 0 ring, cnt <= 32
+template <int CLS>
+__device__ __forceinline__ void lean_batch(LeanShared& S, unsigned pos, unsigned cnt, const InP<double>& in,
+                                           const OutP<double>& out, uint32_t* list, unsigned* count, unsigned lane) {
+  constexpr unsigned ring = CLS == 2 ? kRing2 : kRing0;
+  u64* slots = CLS == 2 ? S.slot2 : S.slot0;
+  if (lane < cnt) {
+    const unsigned p = pos + lane;
+    const unsigned i = q_take(&slots[p & (ring - 1u)], p / ring, 1u + CLS);
+    __threadfence_block();
+    fast_one<double, CLS>(in, out, i, list, count, lane);
+  }
+  __syncwarp();
+}
+// the block runs S.phase queued class 1 indices, 32 per warp (every warp of the block calls this)
+__device__ __forceinline__ void lean_phase1(LeanShared& S, const InP<double>& in, const OutP<double>& out,
+                                            uint32_t* list, unsigned* count, unsigned lane, unsigned wib) {
+  __syncthreads();  // every warp's class 1 entries are in place
+  const unsigned cnt = S.phase, h = S.head1;
+  const unsigned k = 32u * wib + lane;
+  if (k < cnt) fast_one<double, 1>(in, out, S.slot1[(h + k) & (kRing1 - 1u)], list, count, lane);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.head1 = h + cnt;
+    S.phase = S.tail[1] - (h + cnt) >= kPhase1 ? kPhase1 : 0u;
+  }
+  __syncthreads();
+}
+__global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
+    k_svd2_lean(InP<double> in, OutP<double> out, uint64_t n, uint32_t* list, unsigned* count, LeanGlobal* G) {
+  __shared__ LeanShared S;
+  __shared__ double stage[kLeanWarps][2][4][32];
+  for (unsigned k = threadIdx.x; k < sizeof(LeanShared) / sizeof(unsigned); k += blockDim.x)
+    reinterpret_cast<unsigned*>(&S)[k] = 0u;
+  const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  const unsigned n32 = static_cast<unsigned>(n);
+  // the sample: every block reads the same 512 matrices spread over the batch
+  {
+    const uint64_t si = (static_cast<uint64_t>(2u * threadIdx.x + 1u) * n) / (2u * KOG2_FAST_THREADS);
+    const Mat<double> g{in.g11[si], in.g12[si], in.g21[si], in.g22[si]};
+    const unsigned t = type_of(g);
+    const int h11 = hiw(g.g11) & 0x7fffffff, h12 = hiw(g.g12) & 0x7fffffff, h21 = hiw(g.g21) & 0x7fffffff,
+              h22 = hiw(g.g22) & 0x7fffffff;
+    const int hmax = max(max(h11, h12), max(h21, h22)), hmin = min(min(h11, h12), min(h21, h22));
+    const bool sep = hmin >= 0x00100000 && hmax < (2045 << 20) && abs(h11 - h21) >= (28 << 20) &&
+                     abs(h12 - h22) >= (28 << 20);
+    const int ns = __syncthreads_count(sep);  // (also the barrier behind the initialisation of S)
+    // the later tests of svd2_lean fail a few percent more; under ~45% it would not pay
+    if ((ns - ns / 16) * 20 < 9 * KOG2_FAST_THREADS) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) G->mode = 1u;
+      return;
+    }
+    (void)t;
+  }
+  const unsigned below = (1u << lane) - 1u;
+  bool direct = false;  // skip the lean attempt (warp-uniform)
+  unsigned tile = 0;
+  // two chunk numbers ahead: the current one and the next (for the prefetch across the boundary)
+  unsigned chunk = 0, nxt = 0;
+  if (lane == 0) {
+    chunk = atomicAdd(&G->next_chunk, 1u);
+    nxt = atomicAdd(&G->next_chunk, 1u);
+  }
+  chunk = __shfl_sync(0xffffffffu, chunk, 0);
+  unsigned k = 0, stg = 0;
+  unsigned base = chunk * (kLeanChunk * 32u);
+  lean_fetch(stage[wib][0], in, base + lane, n32, lane);
+  bool reported = false, last = false;
+  for (;;) {
+    if (ld_vol(&S.phase) != 0u) {  // (warp-uniform: one shared word)
+      lean_phase1(S, in, out, list, count, lane, wib);
+      continue;
+    }
+    unsigned run = 0, p0 = 0, p2 = 0, c0 = 32u, c2 = 32u;  // batches for this warp: class bits, positions, counts
+    bool through = false;
+    if (base < n32) {
+      // the tile after this one: the next of the chunk, or the first of the next chunk
+      unsigned nbase = base + 32u;
+      if (k + 1u == kLeanChunk) nbase = __shfl_sync(0xffffffffu, nxt, 0) * (kLeanChunk * 32u);
+      lean_fetch(stage[wib][stg ^ 1u], in, nbase + lane, n32, lane);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      const unsigned i = base + lane;
+      const bool probe = (tile % KOG2_LEAN_PROBE) == 0;
+      bool hard = i < n32;
+      unsigned cls = 2;
+      if (hard) {
+        double(*sg)[32] = stage[wib][stg];
+        const Mat<double> g{sg[0][lane], sg[1][lane], sg[2][lane], sg[3][lane]};
+        const unsigned t = type_of(g);
+        // s_type = 0 patterns: 0; t = 15 and one nonzero row or column: 2; else (t ~ 13): 1
+        cls = ((0x0357u >> t) & 1u) ? 0u : (((0x9428u >> t) & 1u) ? 2u : 1u);
+        Result<double> r;
+        if (!direct || probe) {
+          hard = !fast::svd2_lean(g, r);
+        } else {
+          r.u = r.v = g;
+          r.sigma1 = r.sigma2 = EPair<double>{0, 0.0};
+          r.s = 0;
+          r.flags = 0;
+        }
+        store_result<false>(out, i, r);  // queued lanes too: whole sectors at the first touch
+        __threadfence_block();
+      }
+      ++tile;
+      base = nbase;
+      stg ^= 1u;
+      if (++k == kLeanChunk) {
+        k = 0;
+        if (lane == 0) nxt = atomicAdd(&G->next_chunk, 1u);
+      }
+      const unsigned mh = __ballot_sync(0xffffffffu, hard);
+      if (probe) direct = __popc(mh) > 20;  // svd2_lean pays below ~2/3 of the lanes failing
+      if (mh == 0u) continue;
+      const unsigned m0 = __ballot_sync(0xffffffffu, hard && cls == 0u);
+      const unsigned m1 = __ballot_sync(0xffffffffu, hard && cls == 1u);
+      const unsigned m2 = mh & ~(m0 | m1);
+      // lanes 0..2 reserve their class's positions.  Classes 0 and 2: a
+      // reservation that crosses a multiple of 32 makes this warp run the 32
+      // that end there.  Class 1: the reservation that takes the queue to 512
+      // calls the block to a phase.
+      unsigned at = 0, end = 0;
+      bool cross = false;
+      if (lane < 3u) {
+        const unsigned cnt = __popc(lane == 0u ? m0 : (lane == 1u ? m1 : m2));
+        if (cnt != 0u) at = atomicAdd(&S.tail[lane], cnt);
+        end = at + cnt;
+        if (lane == 1u) {
+          const unsigned h = ld_vol(&S.head1);
+          if (end - h >= kPhase1 && at - h < kPhase1) *reinterpret_cast<volatile unsigned*>(&S.phase) = kPhase1;
+        } else {
+          cross = (end >> 5) != (at >> 5);
+        }
+      }
+      run = __ballot_sync(0xffffffffu, cross);
+      p0 = (__shfl_sync(0xffffffffu, end, 0) & ~31u) - 32u;
+      p2 = (__shfl_sync(0xffffffffu, end, 2) & ~31u) - 32u;
+      at = __shfl_sync(0xffffffffu, at, cls);
+      if (hard) {
+        const unsigned mine = cls == 0u ? m0 : (cls == 1u ? m1 : m2);
+        const unsigned at1 = at + __popc(mine & below);
+        if (cls == 1u) {
+          S.slot1[at1 & (kRing1 - 1u)] = i;  // never full: a phase starts at 512 and every warp joins within a tile
+        } else {
+          u64* slot = cls == 2u ? &S.slot2[at1 & (kRing2 - 1u)] : &S.slot0[at1 & (kRing0 - 1u)];
+          q_put(slot, cls == 2u ? at1 / kRing2 : at1 / kRing0, i, 8u + cls);
+        }
+      }
+      __syncwarp();
+    } else {
+      // out of tiles
+      if (!reported) {
+        reported = true;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __threadfence_block();
+        unsigned l = 0;
+        if (lane == 0) l = atomicAdd(&S.done, 1u) == kLeanWarps - 1u;
+        last = __shfl_sync(0xffffffffu, l, 0) != 0u;
+      }
+      if (!last) {  // stand by for phases until the block's last warp is through
+        if (ld_vol(&S.finished) != 0u) break;
+        __nanosleep(100);
+        continue;
+      }
+      // the block's last warp: every other warp has run its batches and stands by
+      __threadfence_block();
+      const unsigned r1 = ld_vol(&S.tail[1]) - ld_vol(&S.head1);
+      if (r1 != 0u) {  // what is left of class 1: more phases (this warp joins at the loop's top)
+        *reinterpret_cast<volatile unsigned*>(&S.phase) = r1 < kPhase1 ? r1 : kPhase1;
+        continue;
+      }
+      const unsigned t2 = ld_vol(&S.tail[2]), t0 = ld_vol(&S.tail[0]);
+      p2 = t2 & ~31u, c2 = t2 & 31u;
+      p0 = t0 & ~31u, c0 = t0 & 31u;
+      run = (c2 ? 4u : 0u) | (c0 ? 1u : 0u);
+      through = true;
+    }
+    if (run & 4u) lean_batch<2>(S, p2, c2, in, out, list, count, lane);
+    if (run & 1u) lean_batch<0>(S, p0, c0, in, out, list, count, lane);
+    if (through) {
+      __threadfence_block();
+      if (lane == 0) *reinterpret_cast<volatile unsigned*>(&S.finished) = 1u;
+      break;
+    }
+  }
+}
+// k_svd2_fast for a batch whose sample sent it back (LeanGlobal::mode)
 #ifdef KOG2_FAST_TMA
 // Experiment (A/B builds only): k_svd2_fast with its input tiles fetched by
 // the bulk-copy engine.  Each warp owns a 32-matrix tile per iteration (the
@@ -227,6 +566,7 @@ __global__ void __launch_bounds__(kThreads, 3)
 }
 
 constexpr uint64_t kFastChunk = 1ull << 31;  // uint32 deferred indices per launch pair
+constexpr uint64_t kLeanMin = 1ull << 22;    // smaller batches: k_svd2_fast alone (the two-speed kernel's start and end cost more)
 
 template <class T, class MatC, class OutC>
 int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* opt, cudaStream_t st) {
@@ -245,10 +585,14 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
       // count (first 256 bytes) and one index per matrix of the largest launch
       // (4 B/matrix against the caller's 96, or 56 for binary32)
       const uint64_t cap = n < kFastChunk ? n : kFastChunk;
-      char* ws = static_cast<char*>(kog2_ws_alloc(256 + cap * sizeof(uint32_t), st));
+      static const bool no_lean = std::getenv("KOG2_SVD2_NO_LEAN") != nullptr;  // A/B comparisons
+      const bool use_lean = sizeof(T) == sizeof(double) && !no_lean && n >= kLeanMin;
+      const size_t list_bytes = (cap * sizeof(uint32_t) + 255) & ~static_cast<size_t>(255);
+      char* ws = static_cast<char*>(kog2_ws_alloc(256 + list_bytes + (use_lean ? sizeof(LeanGlobal) : 0), st));
       if (!ws) return KOG_ERR_CUDA;
       unsigned* count = reinterpret_cast<unsigned*>(ws);
       uint32_t* list = reinterpret_cast<uint32_t*>(ws + 256);
+      LeanGlobal* lg = use_lean ? reinterpret_cast<LeanGlobal*>(ws + 256 + list_bytes) : nullptr;
       const int sms = kog2_sm_count();
       int rc = KOG_OK;
       for (uint64_t lo = 0; lo < n && rc == KOG_OK; lo += kFastChunk) {
@@ -270,8 +614,24 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
                                                                                                count);
         } else
 #endif
+        {
+          const unsigned* gate = nullptr;
+          if constexpr (sizeof(T) == sizeof(double)) {
+            if (lg && len >= kLeanMin) {
+              // resident blocks only (tiles are handed out dynamically); k_svd2_fast behind it runs only
+              // if the kernel's sample sends the batch back
+              if (cudaMemsetAsync(lg, 0, sizeof(LeanGlobal), st) != cudaSuccess) {
+                rc = kog2_cuda_error("cudaMemsetAsync(lean queues)");
+                break;
+              }
+              k_svd2_lean<<<sms * KOG2_FAST_MINB, KOG2_FAST_THREADS, 0, st>>>(ip, ol, len, list, count, lg);
+              if ((rc = launched("k_svd2_lean")) != KOG_OK) break;
+              gate = &lg->mode;
+            }
+          }
           k_svd2_fast<T><<<grid_for(len, FastShape<T>::threads), FastShape<T>::threads, 0, st>>>(ip, ol, len, list,
-                                                                                           count);
+                                                                                           count, gate);
+        }
         if ((rc = launched("k_svd2_fast")) != KOG_OK) break;
         // deferred lanes are rare (none in 2^22-matrix samples of configs 1-5):
         // two blocks per SM drain a list of any length (grid-stride)
@@ -310,6 +670,15 @@ int kog2_fast_stats(unsigned long long* out, int reset) {
     cudaMemcpyToSymbol(kog2::fast::g_kog2_div_site, z, sizeof(kog2::fast::g_kog2_div_site));
   }
   return KOG_OK;
+}
+#endif
+
+#ifdef KOG2_LEAN_DEBUG
+int kog2_lean_debug_host(unsigned* pinned) {
+  return cudaMemcpyToSymbol(g_lean_host, &pinned, sizeof(pinned)) == cudaSuccess ? 0 : -1;
+}
+int kog2_lean_debug(unsigned* out) {
+  return cudaMemcpyFromSymbol(out, g_lean_dbg, sizeof(g_lean_dbg)) == cudaSuccess ? 0 : -1;
 }
 #endif
 
