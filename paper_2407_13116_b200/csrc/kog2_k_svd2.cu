@@ -235,6 +235,8 @@ __device__ __forceinline__ unsigned q_take(u64* slot, unsigned lap, unsigned sit
   *vs = q_word(2u * lap + 2u, 0u);
   return static_cast<unsigned>(w);
 }
+// launches the sample kept on this kernel (diagnostics: kog_svd2_lean_count)
+__device__ unsigned long long g_kog2_lean_total = 0;
 constexpr unsigned kLeanWarps = KOG2_FAST_THREADS / 32;
 constexpr unsigned kRing2 = 512;    // class 2 ring, a power of two
 constexpr unsigned kRing0 = 256;    // class 0 ring
@@ -270,27 +272,43 @@ __device__ __forceinline__ void lean_fetch(double (*st)[32], const InP<double>& 
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
+// The class routes are out-of-line calls: inlined, their register demand pushed
+// the tile loop's own state (tile counters, queue positions) into local memory
+// for the whole loop — a tenth of the kernel's stall samples were reloads of
+// those words.  The batch pointers travel through shared memory (an ABI call
+// would pass fourteen pointers in registers).
+struct LeanParams {
+  InP<double> in;
+  OutP<double> out;
+  uint32_t* list;
+  unsigned* count;
+};
+template <int CLS>
+__device__ __noinline__ void fast_call(const LeanParams* P, unsigned i, unsigned lane) {
+  fast_one<double, CLS>(P->in, P->out, i, P->list, P->count, lane);
+}
 // run the queued indices [pos, pos + cnt) of the class 2 or class 0 ring, cnt <= 32
 template <int CLS>
-__device__ __forceinline__ void lean_batch(LeanShared& S, unsigned pos, unsigned cnt, const InP<double>& in,
-                                           const OutP<double>& out, uint32_t* list, unsigned* count, unsigned lane) {
+__device__ __forceinline__ void lean_batch(LeanShared& S, unsigned pos, unsigned cnt, const LeanParams* P,
+                                           unsigned lane) {
   constexpr unsigned ring = CLS == 2 ? kRing2 : kRing0;
   u64* slots = CLS == 2 ? S.slot2 : S.slot0;
   if (lane < cnt) {
     const unsigned p = pos + lane;
     const unsigned i = q_take(&slots[p & (ring - 1u)], p / ring, 1u + CLS);
     __threadfence_block();
-    fast_one<double, CLS>(in, out, i, list, count, lane);
+    fast_call<CLS>(P, i, lane);
   }
   __syncwarp();
 }
 // the block runs S.phase queued class 1 indices, 32 per warp (every warp of the block calls this)
-__device__ __forceinline__ void lean_phase1(LeanShared& S, const InP<double>& in, const OutP<double>& out,
-                                            uint32_t* list, unsigned* count, unsigned lane, unsigned wib) {
+__device__ __forceinline__ void lean_phase1(LeanShared& S, const LeanParams* P, unsigned lane, unsigned wib) {
   __syncthreads();  // every warp's class 1 entries are in place
   const unsigned cnt = S.phase, h = S.head1;
   const unsigned k = 32u * wib + lane;
-  if (k < cnt) fast_one<double, 1>(in, out, S.slot1[(h + k) & (kRing1 - 1u)], list, count, lane);
+#ifndef KOG2_LEAN_SKIP01
+  if (k < cnt) fast_call<1>(P, S.slot1[(h + k) & (kRing1 - 1u)], lane);
+#endif
   __syncthreads();
   if (threadIdx.x == 0) {
     S.head1 = h + cnt;
@@ -301,16 +319,17 @@ __device__ __forceinline__ void lean_phase1(LeanShared& S, const InP<double>& in
 __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
     k_svd2_lean(InP<double> in, OutP<double> out, uint64_t n, uint32_t* list, unsigned* count, LeanGlobal* G) {
   __shared__ LeanShared S;
+  __shared__ LeanParams SP;
   __shared__ double stage[kLeanWarps][2][4][32];
   for (unsigned k = threadIdx.x; k < sizeof(LeanShared) / sizeof(unsigned); k += blockDim.x)
     reinterpret_cast<unsigned*>(&S)[k] = 0u;
+  if (threadIdx.x == 0) SP = LeanParams{in, out, list, count};
   const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
   const unsigned n32 = static_cast<unsigned>(n);
   // the sample: every block reads the same 512 matrices spread over the batch
   {
     const uint64_t si = (static_cast<uint64_t>(2u * threadIdx.x + 1u) * n) / (2u * KOG2_FAST_THREADS);
     const Mat<double> g{in.g11[si], in.g12[si], in.g21[si], in.g22[si]};
-    const unsigned t = type_of(g);
     const int h11 = hiw(g.g11) & 0x7fffffff, h12 = hiw(g.g12) & 0x7fffffff, h21 = hiw(g.g21) & 0x7fffffff,
               h22 = hiw(g.g22) & 0x7fffffff;
     const int hmax = max(max(h11, h12), max(h21, h22)), hmin = min(min(h11, h12), min(h21, h22));
@@ -322,9 +341,8 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
       if (blockIdx.x == 0 && threadIdx.x == 0) G->mode = 1u;
       return;
     }
-    (void)t;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_kog2_lean_total, 1ull);
   }
-  const unsigned below = (1u << lane) - 1u;
   bool direct = false;  // skip the lean attempt (warp-uniform)
   unsigned tile = 0;
   // two chunk numbers ahead: the current one and the next (for the prefetch across the boundary)
@@ -334,13 +352,12 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
     nxt = atomicAdd(&G->next_chunk, 1u);
   }
   chunk = __shfl_sync(0xffffffffu, chunk, 0);
-  unsigned k = 0, stg = 0;
   unsigned base = chunk * (kLeanChunk * 32u);
   lean_fetch(stage[wib][0], in, base + lane, n32, lane);
   bool reported = false, last = false;
   for (;;) {
     if (ld_vol(&S.phase) != 0u) {  // (warp-uniform: one shared word)
-      lean_phase1(S, in, out, list, count, lane, wib);
+      lean_phase1(S, &SP, lane, threadIdx.x >> 5);
       continue;
     }
     unsigned run = 0, p0 = 0, p2 = 0, c0 = 32u, c2 = 32u;  // batches for this warp: class bits, positions, counts
@@ -348,6 +365,7 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
     if (base < n32) {
       // the tile after this one: the next of the chunk, or the first of the next chunk
       unsigned nbase = base + 32u;
+      const unsigned k = tile % kLeanChunk, stg = tile & 1u;  // tile in its chunk, staging buffer
       if (k + 1u == kLeanChunk) nbase = __shfl_sync(0xffffffffu, nxt, 0) * (kLeanChunk * 32u);
       lean_fetch(stage[wib][stg ^ 1u], in, nbase + lane, n32, lane);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -375,11 +393,7 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
       }
       ++tile;
       base = nbase;
-      stg ^= 1u;
-      if (++k == kLeanChunk) {
-        k = 0;
-        if (lane == 0) nxt = atomicAdd(&G->next_chunk, 1u);
-      }
+      if (k + 1u == kLeanChunk && lane == 0) nxt = atomicAdd(&G->next_chunk, 1u);
       const unsigned mh = __ballot_sync(0xffffffffu, hard);
       if (probe) direct = __popc(mh) > 20;  // svd2_lean pays below ~2/3 of the lanes failing
       if (mh == 0u) continue;
@@ -409,7 +423,7 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
       at = __shfl_sync(0xffffffffu, at, cls);
       if (hard) {
         const unsigned mine = cls == 0u ? m0 : (cls == 1u ? m1 : m2);
-        const unsigned at1 = at + __popc(mine & below);
+        const unsigned at1 = at + __popc(mine & ((1u << lane) - 1u));
         if (cls == 1u) {
           S.slot1[at1 & (kRing1 - 1u)] = i;  // never full: a phase starts at 512 and every warp joins within a tile
         } else {
@@ -446,8 +460,12 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
       run = (c2 ? 4u : 0u) | (c0 ? 1u : 0u);
       through = true;
     }
-    if (run & 4u) lean_batch<2>(S, p2, c2, in, out, list, count, lane);
-    if (run & 1u) lean_batch<0>(S, p0, c0, in, out, list, count, lane);
+    if (run & 4u) lean_batch<2>(S, p2, c2, &SP, lane);
+#ifndef KOG2_LEAN_SKIP01
+    if (run & 1u) lean_batch<0>(S, p0, c0, &SP, lane);
+#else
+    if (run & 1u) for (unsigned q = lane; q < kRing0; q += 32) S.slot0[q] = q_word(2u * (p0 / kRing0 + 1u), 0u);
+#endif
     if (through) {
       __threadfence_block();
       if (lane == 0) *reinterpret_cast<volatile unsigned*>(&S.finished) = 1u;
@@ -686,6 +704,15 @@ int64_t kog_svd2_deferred_count(void) {
   unsigned long long c = 0;
   if (cudaMemcpyFromSymbol(&c, g_kog2_deferred_total, sizeof c) != cudaSuccess) {
     kog2_cuda_error("cudaMemcpyFromSymbol(deferred total)");
+    return -1;
+  }
+  return static_cast<int64_t>(c);
+}
+
+int64_t kog_svd2_lean_count(void) {
+  unsigned long long c = 0;
+  if (cudaMemcpyFromSymbol(&c, g_kog2_lean_total, sizeof c) != cudaSuccess) {
+    kog2_cuda_error("cudaMemcpyFromSymbol(lean total)");
     return -1;
   }
   return static_cast<int64_t>(c);

@@ -1,0 +1,103 @@
+"""The two-speed binary64 decomposition kernel (k_svd2_lean, batches of 2^22
+and more with the default Options): every route through its queues against the
+reference's svd2 (svd2.hpp:603-687), bit for bit — mixed batches whose regions
+change the class mix under the warps' feet (lean-friendly, triangular, narrow
+range, sparse, deferring), ragged sizes, the sample's hand-back to
+k_svd2_fast, several launches in flight."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import refbind
+from paper_2407_13116_b200 import capi, configs
+from paper_2407_13116_b200 import kogsvd2 as K
+from tests import _gen
+from tests.test_gpu_parity import compare_svd, dev, host
+from tests.test_gpu_reentrancy import deferring_batch
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg_host(k: int, n: int, off: int = 0) -> np.ndarray:
+    """(4, n) host matrices of a BASELINE config's generator"""
+    return host(K.generate(configs.cfg(k, count=off + n), off, n))
+
+
+def sparse(seed: int, n: int) -> np.ndarray:
+    """config-3 entries with every zero pattern equally likely (the all-zero matrix included)"""
+    g = cfg_host(3, n, 1 << 20)
+    mask = (_gen.draws(seed, n, 0) % np.uint64(16)).astype(np.int64)
+    for k, bit in enumerate((1, 4, 2, 8)):
+        g[k][(mask & bit) == 0] = 0
+    return g
+
+
+def mixed_batch(n: int, order: int) -> np.ndarray:
+    """about 70% lean-friendly matrices (so that the kernel's sample keeps the
+    batch) cut by stretches of every other kind, in pieces of uneven lengths"""
+    pieces = []
+    left = n
+    k = 0
+    kinds = [3, "tri", 3, "circ", 3, "sparse", 3, "defer", 3, 3, "tri", 3][order:] + [3]
+    sizes = {3: 311_111, "tri": 70_001, "circ": 65_537, "sparse": 50_021, "defer": 40_009}
+    while left > 0:
+        kind = kinds[k % len(kinds)]
+        m = min(left, sizes[kind] + 977 * k)
+        if kind == 3:
+            pieces.append(cfg_host(3, m, 12345 * k))
+        elif kind == "tri":
+            pieces.append(cfg_host(2, m, 999 * k))
+        elif kind == "circ":
+            pieces.append(cfg_host(1, m, 77 * k))
+        elif kind == "sparse":
+            pieces.append(sparse(0x51 + k, m))
+        else:
+            pieces.append(deferring_batch(np.float64, 0xDE00 + k, m))
+        left -= m
+        k += 1
+    return np.ascontiguousarray(np.concatenate(pieces, axis=1))
+
+
+@pytest.mark.parametrize("n,order", [((1 << 22) + (1 << 20) + 37, 0), ((1 << 22) + 1, 3), (3 * (1 << 21) + 31, 1)])
+def test_lean_kernel_mixed_batches(cuda, ref, n, order):
+    g = mixed_batch(n, order)
+    lib = capi.load()
+    kept0, def0 = lib.kog_svd2_lean_count(), lib.kog_svd2_deferred_count()
+    got = K.svd2(dev(g))
+    torch.cuda.synchronize()
+    assert lib.kog_svd2_lean_count() == kept0 + 1, "the sample handed the batch back: k_svd2_lean did not run"
+    assert lib.kog_svd2_deferred_count() > def0, "no lane reached the general kernel"
+    compare_svd(got, refbind.svd2(ref, g), f"mixed batch n={n}")
+
+
+def test_lean_kernel_hands_unfriendly_batches_back(cuda, ref):
+    """narrow-range, triangular and deferring batches of 2^22: the sample sends
+    them to k_svd2_fast (same results either way)"""
+    n = (1 << 22) + 5
+    for what, g in (("circ", cfg_host(1, n)), ("tri", cfg_host(2, n)), ("defer", deferring_batch(np.float64, 0xAB, n))):
+        kept0 = capi.load().kog_svd2_lean_count()
+        got = K.svd2(dev(g))
+        torch.cuda.synchronize()
+        assert capi.load().kog_svd2_lean_count() == kept0, f"{what}: kept on the two-speed kernel"
+        compare_svd(got, refbind.svd2(ref, g), what)
+
+
+def test_lean_kernel_config3_window_and_streams(cuda, ref):
+    """config 3 at 2^22 + a ragged tail on three streams at once (each launch
+    its own queues and workspace), all equal to the reference"""
+    n = (1 << 22) + 12345
+    gs = [cfg_host(3, n, off) for off in (0, 1 << 24, (1 << 27) + 3)]
+    ds = [dev(g) for g in gs]
+    streams = [torch.cuda.Stream() for _ in ds]
+    torch.cuda.synchronize()
+    kept0 = capi.load().kog_svd2_lean_count()
+    outs = []
+    for d, s in zip(ds, streams):
+        with torch.cuda.stream(s):
+            outs.append(K.svd2(d))
+    torch.cuda.synchronize()
+    assert capi.load().kog_svd2_lean_count() == kept0 + 3
+    for k, (g, r) in enumerate(zip(gs, outs)):
+        compare_svd(r, refbind.svd2(ref, g), f"stream {k}")

@@ -1,6 +1,6 @@
 #!/bin/bash
 # bench kernel line with and without the lean kernel (no tests)
-P=${1:-r3}
+P=${1:-lean}
 for v in lean nolean lean nolean; do
   if [ $v = nolean ]; then export KOG2_SVD2_NO_LEAN=1; else unset KOG2_SVD2_NO_LEAN; fi
   timeout 300 python bench.py --no-e2e --no-study --no-cpu --steps 10 --warmup 3 2>/dev/null | python -c "

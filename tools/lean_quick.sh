@@ -1,6 +1,6 @@
 #!/bin/bash
 # quick GPU check of a kernel change: svd2 parity subsets, then the bench kernel line with and without the lean kernel
-P=${1:-r3q}
+P=${1:-leanq}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_full_parity.py tests/test_gpu_reentrancy.py -m gpu -x -q > gpurun_out/${P}_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${P}_pytest.log
 for v in lean nolean lean nolean; do
