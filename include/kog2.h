@@ -433,6 +433,10 @@ int64_t kog_svd2_deferred_count(void);
  * handing the batch back to k_svd2_fast, on the current device since load
  * (synchronous; -1 on error).  Diagnostics only. */
 int64_t kog_svd2_lean_count(void);
+/* Tuning knob: the smallest kog_svd2_batch_f64 batch (default Options) that is
+ * offered to the two-speed kernel (default 2^24; at least 2^16).  Returns the
+ * previous value.  Results do not depend on it. */
+uint64_t kog_svd2_set_lean_min(uint64_t n);
 /* number of kernel launches issued by this library since load */
 uint64_t kog_launch_count(void);
 

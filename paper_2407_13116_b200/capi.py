@@ -180,6 +180,7 @@ PROTOTYPES: dict[str, tuple] = {
     "kog_fp64_probe": (i32, [P, u64, C.c_uint32, P]),
     "kog_svd2_deferred_count": (C.c_int64, []),
     "kog_svd2_lean_count": (C.c_int64, []),
+    "kog_svd2_set_lean_min": (C.c_uint64, [C.c_uint64]),
     "kog_div_batch_f64": (i32, [P, P, P, u64, P]),
     "kog_div_batch_f32": (i32, [P, P, P, u64, P]),
     "kog_launch_count": (C.c_uint64, []),

@@ -13,6 +13,7 @@
 // binary32 with the default Options takes the same two launches (the
 // binary32 instantiation of kog2_fast.cuh); other Options run the general
 // kernel over the batch.
+#include <atomic>
 #include <cstdlib>
 
 #include "kog2_common.cuh"
@@ -584,7 +585,10 @@ __global__ void __launch_bounds__(kThreads, 3)
 }
 
 constexpr uint64_t kFastChunk = 1ull << 31;  // uint32 deferred indices per launch pair
-constexpr uint64_t kLeanMin = 1ull << 22;    // smaller batches: k_svd2_fast alone (the two-speed kernel's start and end cost more)
+// smaller batches: k_svd2_fast alone — the two-speed kernel's start (sample, queue set-up) and end (partial
+// batches, the blocks' last phases) cost ~50 us; it breaks even near 2^23.5 config-3 matrices
+// (profiles/r3_lean_sizes.txt).  kog_svd2_set_lean_min moves the threshold (tests run the kernel on less).
+static std::atomic<uint64_t> g_lean_min{1ull << 24};
 
 template <class T, class MatC, class OutC>
 int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* opt, cudaStream_t st) {
@@ -604,7 +608,8 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
       // (4 B/matrix against the caller's 96, or 56 for binary32)
       const uint64_t cap = n < kFastChunk ? n : kFastChunk;
       static const bool no_lean = std::getenv("KOG2_SVD2_NO_LEAN") != nullptr;  // A/B comparisons
-      const bool use_lean = sizeof(T) == sizeof(double) && !no_lean && n >= kLeanMin;
+      const uint64_t lean_min = g_lean_min.load(std::memory_order_relaxed);
+      const bool use_lean = sizeof(T) == sizeof(double) && !no_lean && n >= lean_min;
       const size_t list_bytes = (cap * sizeof(uint32_t) + 255) & ~static_cast<size_t>(255);
       char* ws = static_cast<char*>(kog2_ws_alloc(256 + list_bytes + (use_lean ? sizeof(LeanGlobal) : 0), st));
       if (!ws) return KOG_ERR_CUDA;
@@ -635,7 +640,7 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
         {
           const unsigned* gate = nullptr;
           if constexpr (sizeof(T) == sizeof(double)) {
-            if (lg && len >= kLeanMin) {
+            if (lg && len >= lean_min) {
               // resident blocks only (tiles are handed out dynamically); k_svd2_fast behind it runs only
               // if the kernel's sample sends the batch back
               if (cudaMemsetAsync(lg, 0, sizeof(LeanGlobal), st) != cudaSuccess) {
@@ -707,6 +712,10 @@ int64_t kog_svd2_deferred_count(void) {
     return -1;
   }
   return static_cast<int64_t>(c);
+}
+
+uint64_t kog_svd2_set_lean_min(uint64_t n) {
+  return g_lean_min.exchange(n < (1ull << 16) ? (1ull << 16) : n, std::memory_order_relaxed);
 }
 
 int64_t kog_svd2_lean_count(void) {

@@ -20,6 +20,15 @@ from tests.test_gpu_reentrancy import deferring_batch
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def small_batches_on_the_lean_kernel():
+    """the kernel normally takes batches of 2^24 and more; these tests run it on 2^22"""
+    lib = capi.load()
+    before = lib.kog_svd2_set_lean_min(1 << 22)
+    yield
+    lib.kog_svd2_set_lean_min(before)
+
+
 def cfg_host(k: int, n: int, off: int = 0) -> np.ndarray:
     """(4, n) host matrices of a BASELINE config's generator"""
     return host(K.generate(configs.cfg(k, count=off + n), off, n))
