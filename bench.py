@@ -334,6 +334,14 @@ SHAPE_OF = {1: "general (circ)", 2: "upper-triangular (e in [-1000,1000])", 3: "
             4: "general (e in [-60,60], 1% subnormal-adjacent)"}
 
 
+def kernels_of(suf: str, n: int) -> str:
+    """the launches behind one kog_svd2_batch call (csrc/kog2_k_svd2.cu: launch_svd2)"""
+    if suf == "f64" and n >= 1 << 24:
+        return ("k_svd2_lean (two-speed kernel; hands the batch back to the k_svd2_fast launched behind it if "
+                "its input sample says so) + k_svd2_list (one kog_svd2_batch_f64 call)")
+    return f"k_svd2_fast + k_svd2_list (one kog_svd2_batch_{suf} call)"
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -408,7 +416,7 @@ def main() -> None:
     fp64 = fp64_probe(K, torch)
     fp64_ops = fp64["fma_ops_per_s"]
     main_roof = roofline(n / kern_s, bpm, W_SVD2[args.config], pk, fp64_ops, kern_s, traffic.get(args.config),
-                         f"k_svd2_fast + k_svd2_list (one kog_svd2_batch_{suf} call)", n)
+                         kernels_of(suf, n), n)
 
     # ---- the other BASELINE configs' decompositions (parity-test sizes of their own; one GPU each)
     per_config = {}
@@ -436,7 +444,7 @@ def main() -> None:
                 "l2": l2_note(nk * bk) + ("; L2 overwritten (512 MiB write) before every timed call, outside "
                                           "the timed events" if flush is not None else ""),
                 "roofline": roofline(rk, bk, W_SVD2[k], pk, fp64_ops, tk["kernel_s"], traffic.get(k),
-                                     f"k_svd2_fast + k_svd2_list (one kog_svd2_batch_{sk} call)", nk),
+                                     kernels_of(sk, nk), nk),
                 "clocks": tk["clocks"], "gpu_launches": tk["launches"]}
             del gk, ok, flush
             torch.cuda.empty_cache()
