@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
           r.flags = 0;
         }
         store_result<false>(out, i, r);  // queued lanes too: whole sectors at the first touch
-        __threadfence_block();
+        asm volatile("fence.acq_rel.cta;" ::: "memory");  // before the push (lighter than __threadfence_block's fence.sc)
       }
       ++tile;
       base = nbase;
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
       }
       if (!last) {  // stand by for phases until the block's last warp is through
         if (ld_vol(&S.finished) != 0u) break;
-        __nanosleep(100);
+        __nanosleep(500);
         continue;
       }
       // the block's last warp: every other warp has run its batches and stands by

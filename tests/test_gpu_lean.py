@@ -110,3 +110,29 @@ def test_lean_kernel_config3_window_and_streams(cuda, ref):
     assert capi.load().kog_svd2_lean_count() == kept0 + 3
     for k, (g, r) in enumerate(zip(gs, outs)):
         compare_svd(r, refbind.svd2(ref, g), f"stream {k}")
+
+
+def test_lean_kernel_guard_zones(cuda, ref):
+    """the two-speed kernel on arrays carved out of larger allocations (64 KiB
+    guard zones, 8-byte-aligned but not 16-byte-aligned pointers: its cp.async
+    copies are 8 bytes wide) at a ragged size: no write outside the arrays, the
+    inputs unchanged, results equal to the reference"""
+    import ctypes as C
+
+    from tests.test_gpu_guards import Arena, _st
+
+    lib = capi.load()
+    n = (1 << 22) + 4099
+    g = mixed_batch(n, 2)
+    A = Arena()
+    ins = [A.array(n, torch.float64, g[k]) for k in range(4)]
+    outs = {k: A.array(n, torch.int32 if k in ("sig1_e", "sig2_e", "s", "flags") else torch.float64)
+            for k in K.SVD_FIELDS}
+    m = capi.kog_mat(*[t.data_ptr() for t in ins])
+    o = capi.kog_svd_out(*[outs[k].data_ptr() for k in K.SVD_FIELDS])
+    kept0 = lib.kog_svd2_lean_count()
+    opt = capi.default_options()
+    capi.check(lib.kog_svd2_batch_f64(C.byref(m), C.byref(o), n, C.byref(opt), _st()))
+    A.check("k_svd2_lean")
+    assert lib.kog_svd2_lean_count() == kept0 + 1
+    compare_svd(outs, refbind.svd2(ref, g), "guarded two-speed call")
