@@ -350,16 +350,18 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
   // (chunks start at multiples of 256 matrices), and the next chunk is claimed when it is needed (the round
   // trip, once per eight tiles, hides behind the other warps): loop words that the compiler has to keep in
   // local memory around the class calls cost reloads on every tile.
-  bool direct = false;  // skip the lean attempt (warp-uniform)
-  unsigned base = 0;
-  if (lane == 0) base = atomicAdd(&G->next_chunk, 1u);
-  base = __shfl_sync(0xffffffffu, base, 0) * (kLeanChunk * 32u);
-  lean_fetch(stage[wib][0], in, base + lane, n32, lane);
-  while (base < n32) {
+  // (`direct`, warp-uniform: skip the lean attempt, rides in bit 0 of the loop word — bases are multiples of 32)
+  unsigned bd = 0;
+  if (lane == 0) bd = atomicAdd(&G->next_chunk, 1u);
+  bd = __shfl_sync(0xffffffffu, bd, 0) * (kLeanChunk * 32u);
+  lean_fetch(stage[wib][0], in, bd + lane, n32, lane);
+  while ((bd & ~31u) < n32) {
     if (ld_vol(&S.phase) != 0u) {  // (warp-uniform: one shared word)
       lean_phase1(S, &SP, lane, threadIdx.x >> 5);
       continue;
     }
+    const unsigned base = bd & ~31u;
+    bool direct = (bd & 1u) != 0u;
     const unsigned tk = base >> 5;  // tile number: its low bits are the place in the chunk
     unsigned nbase = base + 32u;
     if ((tk & (kLeanChunk - 1u)) == kLeanChunk - 1u) {  // the chunk's last tile: claim the next chunk
@@ -393,9 +395,9 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
       store_result<false>(out, i, r);  // queued lanes too: whole sectors at the first touch
       asm volatile("fence.acq_rel.cta;" ::: "memory");  // before the push (lighter than __threadfence_block's fence.sc)
     }
-    base = nbase;
     const unsigned mh = __ballot_sync(0xffffffffu, hard);
     if (probe) direct = __popc(mh) > 20;  // svd2_lean pays below ~2/3 of the lanes failing
+    bd = nbase | (direct ? 1u : 0u);
     if (mh == 0u) continue;
     const unsigned m0 = __ballot_sync(0xffffffffu, hard && cls == 0u);
     const unsigned m1 = __ballot_sync(0xffffffffu, hard && cls == 1u);
