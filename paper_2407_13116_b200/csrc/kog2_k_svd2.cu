@@ -241,9 +241,13 @@ __device__ unsigned long long g_kog2_lean_total = 0;
 constexpr unsigned kLeanWarps = KOG2_FAST_THREADS / 32;
 constexpr unsigned kRing2 = 512;    // class 2 ring, a power of two
 constexpr unsigned kRing0 = 256;    // class 0 ring
-constexpr unsigned kRing1 = 2048;   // class 1 store (plain words: filled between phases, emptied inside them)
-constexpr unsigned kPhase1 = 32 * kLeanWarps;  // class 1 entries per phase
+#ifndef KOG2_LEAN_PHASE
+#define KOG2_LEAN_PHASE 512  // measured (config 3, ms per 2^28): 128 -> 11.25, 256 -> 10.67, 512 -> 10.51, 1024 -> 10.57, 2048 -> 10.80
+#endif
+constexpr unsigned kPhase1 = KOG2_LEAN_PHASE;  // class 1 entries per phase (32 per warp and round)
+constexpr unsigned kRing1 = kPhase1 < 512 ? 2048 : 4 * kPhase1;  // class 1 store (plain words: filled between phases, emptied inside them)
 constexpr unsigned kLeanChunk = 8;  // consecutive tiles per grab
+constexpr unsigned kLeanStageBytes = kLeanWarps * 2 * 4 * 32 * sizeof(double);  // dynamic shared memory of k_svd2_lean
 struct LeanGlobal {
   unsigned next_chunk;
   unsigned mode;  // 1: the batch goes to k_svd2_fast
@@ -302,14 +306,13 @@ __device__ __forceinline__ void lean_batch(LeanShared& S, unsigned pos, unsigned
   }
   __syncwarp();
 }
-// the block runs S.phase queued class 1 indices, 32 per warp (every warp of the block calls this)
+// the block runs S.phase queued class 1 indices, 32 per warp and round (every warp of the block calls this)
 __device__ __forceinline__ void lean_phase1(LeanShared& S, const LeanParams* P, unsigned lane, unsigned wib) {
   __syncthreads();  // every warp's class 1 entries are in place
   const unsigned cnt = S.phase, h = S.head1;
-  const unsigned k = 32u * wib + lane;
-#ifndef KOG2_LEAN_SKIP01
-  if (k < cnt) fast_call<1>(P, S.slot1[(h + k) & (kRing1 - 1u)], lane);
-#endif
+#pragma unroll 1
+  for (unsigned k = 32u * wib + lane; k < cnt; k += 32u * kLeanWarps)
+    fast_call<1>(P, S.slot1[(h + k) & (kRing1 - 1u)], lane);
   __syncthreads();
   if (threadIdx.x == 0) {
     S.head1 = h + cnt;
@@ -321,7 +324,8 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
     k_svd2_lean(InP<double> in, OutP<double> out, uint64_t n, uint32_t* list, unsigned* count, LeanGlobal* G) {
   __shared__ LeanShared S;
   __shared__ LeanParams SP;
-  __shared__ double stage[kLeanWarps][2][4][32];
+  extern __shared__ __align__(16) unsigned char lean_dyn[];  // the input staging buffers (kLeanStageBytes)
+  double(*stage)[2][4][32] = reinterpret_cast<double(*)[2][4][32]>(lean_dyn);
   for (unsigned k = threadIdx.x; k < sizeof(LeanShared) / sizeof(unsigned); k += blockDim.x)
     reinterpret_cast<unsigned*>(&S)[k] = 0u;
   if (threadIdx.x == 0) SP = LeanParams{in, out, list, count};
@@ -640,7 +644,13 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
                 rc = kog2_cuda_error("cudaMemsetAsync(lean queues)");
                 break;
               }
-              k_svd2_lean<<<sms * KOG2_FAST_MINB, KOG2_FAST_THREADS, 0, st>>>(ip, ol, len, list, count, lg);
+              static const bool smem_ok = cudaFuncSetAttribute(k_svd2_lean, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                               static_cast<int>(kLeanStageBytes)) == cudaSuccess;
+              if (!smem_ok) {
+                rc = kog2_cuda_error("cudaFuncSetAttribute(k_svd2_lean)");
+                break;
+              }
+              k_svd2_lean<<<sms * KOG2_FAST_MINB, KOG2_FAST_THREADS, kLeanStageBytes, st>>>(ip, ol, len, list, count, lg);
               if ((rc = launched("k_svd2_lean")) != KOG_OK) break;
               gate = &lg->mode;
             }
