@@ -159,14 +159,14 @@ __device__ __forceinline__ void fast_one(const InP<T>& in, const OutP<T>& out, u
 //   class 2  t = 15 and the one-row/column patterns that ride along urv15,
 //   class 0  svd_simple patterns: the warp whose push takes the queue across a
 //            multiple of 32 runs svd2_fast<2> (svd2_fast<0>) over those 32;
-//   class 1  t ~ 13: run by the whole block at once whenever 512 are queued
+//   class 1  t ~ 13: run by the whole block at once whenever 32 per warp are queued
 //            (phase1: every warp takes 32), because its code is a quarter of
 //            the kernel's and the SM's instruction cache holds 32 KB — with
 //            every warp running every class whenever its push completed a
 //            batch, the kernel spent a quarter of its time waiting for
 //            instructions (profiles/r3_icache.txt); this way the other
 //            classes' 38 KB stay resident between phases.
-// The block's sixteen warps fill a batch of classes 2 and 0 within a tile or
+// The block's thirty-two warps fill a batch of classes 2 and 0 within a tile or
 // two, so the queued matrices' inputs and the output sectors they share with
 // their neighbours are still in L2 when the batch runs.  Queue slots are
 // exact-turn words (q_put / q_take above); no block waits for another, and
@@ -236,13 +236,23 @@ __device__ __forceinline__ unsigned q_take(u64* slot, unsigned lap, unsigned sit
   *vs = q_word(2u * lap + 2u, 0u);
   return static_cast<unsigned>(w);
 }
+// Block shape: one block of 1024 threads per SM.  Thirty-two warps on one set of queues fill a batch twice as
+// fast as sixteen (the queued matrices' sectors are younger in L2) and the SM holds one hot code set instead of
+// two blocks' worth.  Measured (config 3, ms per 2^28, class 1 phase = 32 per warp): 256 x 4: 10.65,
+// 512 x 2: 10.51, 1024 x 1: 10.04 (phase 512: 10.57, 2048: 10.17).
+#ifndef KOG2_LEAN_THREADS
+#define KOG2_LEAN_THREADS 1024
+#endif
+#ifndef KOG2_LEAN_MINB
+#define KOG2_LEAN_MINB 1
+#endif
 // launches the sample kept on this kernel (diagnostics: kog_svd2_lean_count)
 __device__ unsigned long long g_kog2_lean_total = 0;
-constexpr unsigned kLeanWarps = KOG2_FAST_THREADS / 32;
+constexpr unsigned kLeanWarps = KOG2_LEAN_THREADS / 32;
 constexpr unsigned kRing2 = 512;    // class 2 ring, a power of two
 constexpr unsigned kRing0 = 256;    // class 0 ring
 #ifndef KOG2_LEAN_PHASE
-#define KOG2_LEAN_PHASE 512  // measured (config 3, ms per 2^28): 128 -> 11.25, 256 -> 10.67, 512 -> 10.51, 1024 -> 10.57, 2048 -> 10.80
+#define KOG2_LEAN_PHASE (KOG2_LEAN_THREADS)  // 32 per warp; measured at 512 threads (config 3, ms per 2^28): 128 -> 11.25, 256 -> 10.67, 512 -> 10.51, 1024 -> 10.57, 2048 -> 10.80
 #endif
 constexpr unsigned kPhase1 = KOG2_LEAN_PHASE;  // class 1 entries per phase (32 per warp and round)
 constexpr unsigned kRing1 = kPhase1 < 512 ? 2048 : 4 * kPhase1;  // class 1 store (plain words: filled between phases, emptied inside them)
@@ -320,7 +330,7 @@ __device__ __forceinline__ void lean_phase1(LeanShared& S, const LeanParams* P, 
   }
   __syncthreads();
 }
-__global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
+__global__ void __launch_bounds__(KOG2_LEAN_THREADS, KOG2_LEAN_MINB)
     k_svd2_lean(InP<double> in, OutP<double> out, uint64_t n, uint32_t* list, unsigned* count, LeanGlobal* G) {
   __shared__ LeanShared S;
   __shared__ LeanParams SP;
@@ -333,7 +343,7 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
   const unsigned n32 = static_cast<unsigned>(n);
   // the sample: every block reads the same 512 matrices spread over the batch
   {
-    const uint64_t si = (static_cast<uint64_t>(2u * threadIdx.x + 1u) * n) / (2u * KOG2_FAST_THREADS);
+    const uint64_t si = (static_cast<uint64_t>(2u * threadIdx.x + 1u) * n) / (2u * KOG2_LEAN_THREADS);
     const Mat<double> g{in.g11[si], in.g12[si], in.g21[si], in.g22[si]};
     const int h11 = hiw(g.g11) & 0x7fffffff, h12 = hiw(g.g12) & 0x7fffffff, h21 = hiw(g.g21) & 0x7fffffff,
               h22 = hiw(g.g22) & 0x7fffffff;
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(KOG2_FAST_THREADS, KOG2_FAST_MINB)
                      abs(h12 - h22) >= (28 << 20);
     const int ns = __syncthreads_count(sep);  // (also the barrier behind the initialisation of S)
     // the later tests of svd2_lean fail a few percent more; under ~45% it would not pay
-    if ((ns - ns / 16) * 20 < 9 * KOG2_FAST_THREADS) {
+    if ((ns - ns / 16) * 20 < 9 * KOG2_LEAN_THREADS) {
       if (blockIdx.x == 0 && threadIdx.x == 0) G->mode = 1u;
       return;
     }
@@ -650,7 +660,7 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
                 rc = kog2_cuda_error("cudaFuncSetAttribute(k_svd2_lean)");
                 break;
               }
-              k_svd2_lean<<<sms * KOG2_FAST_MINB, KOG2_FAST_THREADS, kLeanStageBytes, st>>>(ip, ol, len, list, count, lg);
+              k_svd2_lean<<<sms * KOG2_LEAN_MINB, KOG2_LEAN_THREADS, kLeanStageBytes, st>>>(ip, ol, len, list, count, lg);
               if ((rc = launched("k_svd2_lean")) != KOG_OK) break;
               gate = &lg->mode;
             }
