@@ -249,14 +249,20 @@ __device__ __forceinline__ unsigned q_take(u64* slot, unsigned lap, unsigned sit
 // launches the sample kept on this kernel (diagnostics: kog_svd2_lean_count)
 __device__ unsigned long long g_kog2_lean_total = 0;
 constexpr unsigned kLeanWarps = KOG2_LEAN_THREADS / 32;
-constexpr unsigned kRing2 = 512;    // class 2 ring, a power of two
+#ifndef KOG2_LEAN_RING2
+#define KOG2_LEAN_RING2 512
+#endif
+#ifndef KOG2_LEAN_CHUNK
+#define KOG2_LEAN_CHUNK 8
+#endif
+constexpr unsigned kRing2 = KOG2_LEAN_RING2;    // class 2 ring, a power of two
 constexpr unsigned kRing0 = 256;    // class 0 ring
 #ifndef KOG2_LEAN_PHASE
 #define KOG2_LEAN_PHASE (KOG2_LEAN_THREADS)  // 32 per warp; measured at 512 threads (config 3, ms per 2^28): 128 -> 11.25, 256 -> 10.67, 512 -> 10.51, 1024 -> 10.57, 2048 -> 10.80
 #endif
 constexpr unsigned kPhase1 = KOG2_LEAN_PHASE;  // class 1 entries per phase (32 per warp and round)
 constexpr unsigned kRing1 = kPhase1 < 512 ? 2048 : 4 * kPhase1;  // class 1 store (plain words: filled between phases, emptied inside them)
-constexpr unsigned kLeanChunk = 8;  // consecutive tiles per grab
+constexpr unsigned kLeanChunk = KOG2_LEAN_CHUNK;  // consecutive tiles per grab (a power of two, even)
 constexpr unsigned kLeanStageBytes = kLeanWarps * 2 * 4 * 32 * sizeof(double);  // dynamic shared memory of k_svd2_lean
 struct LeanGlobal {
   unsigned next_chunk;

@@ -4,10 +4,11 @@
 // own early-out and most quotients are divisions by 1.
 //
 // On inputs whose exponents are spread over hundreds of binades (configs 3
-// and 5: e uniform in [-500, 500]) about 86% of the full matrices are like
-// this: the two entries of each column lie 28 binades or more apart, so do
-// r11 and r12, and tan(2 phi), tan(psi) and the composed tangent are below
-// 2^-27.  Then, with the same bits as the reference:
+// and 5: e uniform in [-500, 500]) about 90% of the full matrices are like
+// this: the two entries of the pivot column lie 28 binades or more apart (the
+// other column's too, or it is clearly the smaller one), so do r11 and r12,
+// and tan(2 phi), tan(psi) and the composed tangent are below 2^-27.  Then,
+// with the same bits as the reference:
 //   * hypot_cr(a, b) = max(|a|, |b|) (fpcore.hpp:150 and hypot_args, kog2_fp.cuh);
 //   * sec(theta) = sec(phi) = sec(psi) = sec(chi) = hypot_cr(t, 1) = 1 for |t| < 2^-27
 //     (1 <= sqrt(1 + t^2) < 1 + 2^-55, half an ulp of 1 is 2^-53), so every x / sec
@@ -45,11 +46,17 @@ __device__ __forceinline__ bool svd2_lean(const Mat<double>& gi, Result<double>&
   bool bad = hmin < 0x00100000 || hmax >= (2045 << 20);
   const int s = 2044 - (hmax >> 20);
   const int sh = s << 20;
-  // urv15's column norms (svd2.hpp:343-344): the early-out of hypot_args on
-  // both columns (high words 28 binades or more apart) — each norm is the
-  // column's larger entry
+  // urv15's column norms (svd2.hpp:343-344): the early-out of hypot_args (high
+  // words 28 binades or more apart) — the norm is the column's larger entry
   const int d1 = h11 - h21, d2 = h12 - h22;
-  bad |= abs(d1) < (28 << 20) || abs(d2) < (28 << 20);
+  // The pivot column's norm must be its larger entry.  The OTHER column's norm only decides the column
+  // exchange (w1 < w2, svd2.hpp:345): a column whose entries lie within 28 binades of each other may stay if it
+  // surely is not the pivot column — its correctly rounded norm is at most sqrt 2 (1 + 2^-53) times its larger
+  // entry, and that is below the other column's larger entry (= norm) when the high words are 2^20 apart (a
+  // factor 2 (1 - 2^-20) or more), so comparing the larger entries decides w1 < w2 as the norms would.
+  const bool near1 = abs(d1) < (28 << 20), near2 = abs(d2) < (28 << 20);
+  const int m1 = max(h11, h21), m2 = max(h12, h22);
+  bad |= (near1 && (near2 || m2 - m1 < (1 << 20))) || (near2 && m1 - m2 < (1 << 20));
   const bool lo1 = d1 < 0, lo2 = d2 < 0;  // the column's larger entry sits in row 1
   const bool col_swap = fabs(lo1 ? gi.g21 : gi.g11) < fabs(lo2 ? gi.g22 : gi.g12);
   // the pivot column (cx, cy) and the other one (ox, oy); row signs make the
