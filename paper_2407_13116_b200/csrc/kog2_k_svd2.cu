@@ -660,8 +660,9 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
                 rc = kog2_cuda_error("cudaMemsetAsync(lean queues)");
                 break;
               }
-              static const bool smem_ok = cudaFuncSetAttribute(k_svd2_lean, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                               static_cast<int>(kLeanStageBytes)) == cudaSuccess;
+              // (per device, so on every launch: microseconds against a kernel of a millisecond and more)
+              const bool smem_ok = cudaFuncSetAttribute(k_svd2_lean, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        static_cast<int>(kLeanStageBytes)) == cudaSuccess;
               if (!smem_ok) {
                 rc = kog2_cuda_error("cudaFuncSetAttribute(k_svd2_lean)");
                 break;
