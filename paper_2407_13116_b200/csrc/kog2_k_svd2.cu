@@ -153,31 +153,34 @@ __device__ __forceinline__ void fast_one(const InP<T>& in, const OutP<T>& out, u
 //
 // Each warp walks 32-matrix tiles through svd2_lean (kog2_lean.cuh: the
 // separated t' = 15 case, about a third of svd2_fast's instructions) and
-// sorts the lanes it does not cover into three queues in the block's shared
-// memory, by zero pattern, so that the rest of the work runs as full warps on
-// one route each:
-//   class 2  t = 15 and the one-row/column patterns that ride along urv15,
-//   class 0  svd_simple patterns: the warp whose push takes the queue across a
-//            multiple of 32 runs svd2_fast<2> (svd2_fast<0>) over those 32;
-//   class 1  t ~ 13: run by the whole block at once whenever 32 per warp are queued
-//            (phase1: every warp takes 32), because its code is a quarter of
-//            the kernel's and the SM's instruction cache holds 32 KB — with
-//            every warp running every class whenever its push completed a
-//            batch, the kernel spent a quarter of its time waiting for
-//            instructions (profiles/r3_icache.txt); this way the other
-//            classes' 38 KB stay resident between phases.
-// The block's thirty-two warps fill a batch of classes 2 and 0 within a tile or
-// two, so the queued matrices' inputs and the output sectors they share with
-// their neighbours are still in L2 when the batch runs.  Queue slots are
-// exact-turn words (q_put / q_take above); no block waits for another, and
-// tiles are handed out dynamically, eight consecutive tiles per grab.
+// sorts the lanes it does not cover into two queues in the block's shared
+// memory, so that the rest of the work runs as full warps on one kind of
+// route each:
+//   class T  every pattern that goes through a triangle (t = 15, t ~ 13 and the
+//            one-row/column patterns that ride along urv15): svd2_fast<3>;
+//   class S  svd_simple patterns: svd2_fast<0>.
+// The warp whose push takes a queue across a multiple of 32 runs those 32.
+// (A single queue ran at 12 of 32 lanes: the queue concentrates the divergent
+// lanes, and svd_simple lanes leave at once.  A third queue for t ~ 13, run by
+// the whole block in phases to keep its 16 KB of code out of the 32 KB
+// instruction cache, cost 14% of the kernel's time for 3% of the matrices in
+// barriers, cold code and far-away output sectors; sharing the class T
+// instance costs those lanes' warps ~100 more instructions per batch instead.
+// profiles/r3_lean_kernel_notes.txt has the numbers of every step.)
+// The block's thirty-two warps (one block of 1024 threads per SM) fill a batch
+// within a fraction of a tile, so the queued matrices' inputs and the output
+// sectors they share with their neighbours are still in L2 when the batch
+// runs; with a queue per warp they had long left it.  Queue slots are
+// exact-turn words (q_put / q_take below); no warp waits for anything but a
+// running warp's next step, no block waits for another, and tiles are handed
+// out dynamically, eight consecutive tiles per grab.
 // Outputs: a sector must be written whole the first time (a first partial
 // write costs a DRAM fill read and a second write-back), so the lanes that are
 // queued store their (meaningless) lean result too and their batch overwrites
 // it a moment later; the fences order the two stores.  The next tile's inputs
 // are copied to shared memory while the current one is computed (cp.async).
-// A batch whose 512-matrix sample says svd2_lean would fail on more than about
-// half the matrices sets LeanGlobal::mode and leaves the whole batch to
+// A batch whose 1024-matrix sample says svd2_lean would fail on more than
+// about half the matrices sets LeanGlobal::mode and leaves the whole batch to
 // k_svd2_fast, launched behind it.
 #ifndef KOG2_LEAN_PROBE
 #define KOG2_LEAN_PROBE 16
@@ -248,56 +251,62 @@ __device__ __forceinline__ unsigned q_take(u64* slot, unsigned lap, unsigned sit
 #endif
 // launches the sample kept on this kernel (diagnostics: kog_svd2_lean_count)
 __device__ unsigned long long g_kog2_lean_total = 0;
-constexpr unsigned kLeanWarps = KOG2_LEAN_THREADS / 32;
-#ifndef KOG2_LEAN_RING2
-#define KOG2_LEAN_RING2 512
+// Block shape: one block of 1024 threads per SM.  Thirty-two warps on one set of queues fill a batch twice as
+// fast as sixteen (the queued matrices' sectors are younger in L2) and the SM holds one hot code set instead of
+// two blocks' worth.  Measured (config 3, ms per 2^28): 256 x 4: 10.65, 512 x 2: 10.51, 1024 x 1: 10.04.
+#ifndef KOG2_LEAN_THREADS
+#define KOG2_LEAN_THREADS 1024
+#endif
+#ifndef KOG2_LEAN_MINB
+#define KOG2_LEAN_MINB 1
+#endif
+#ifndef KOG2_LEAN_RINGT
+#define KOG2_LEAN_RINGT 512
 #endif
 #ifndef KOG2_LEAN_CHUNK
 #define KOG2_LEAN_CHUNK 8
 #endif
-constexpr unsigned kRing2 = KOG2_LEAN_RING2;    // class 2 ring, a power of two
-constexpr unsigned kRing0 = 256;    // class 0 ring
-#ifndef KOG2_LEAN_PHASE
-#define KOG2_LEAN_PHASE (KOG2_LEAN_THREADS)  // 32 per warp; measured at 512 threads (config 3, ms per 2^28): 128 -> 11.25, 256 -> 10.67, 512 -> 10.51, 1024 -> 10.57, 2048 -> 10.80
-#endif
-constexpr unsigned kPhase1 = KOG2_LEAN_PHASE;  // class 1 entries per phase (32 per warp and round)
-constexpr unsigned kRing1 = kPhase1 < 512 ? 2048 : 4 * kPhase1;  // class 1 store (plain words: filled between phases, emptied inside them)
-constexpr unsigned kLeanChunk = KOG2_LEAN_CHUNK;  // consecutive tiles per grab (a power of two, even)
+constexpr unsigned kLeanWarps = KOG2_LEAN_THREADS / 32;
+constexpr unsigned kRingT = KOG2_LEAN_RINGT;  // class T ring, a power of two (512 .. 2048 measured alike)
+constexpr unsigned kRingS = 256;              // class S ring
+constexpr unsigned kLeanChunk = KOG2_LEAN_CHUNK;  // consecutive tiles per grab (a power of two, even; 4 .. 16 measured alike)
 constexpr unsigned kLeanStageBytes = kLeanWarps * 2 * 4 * 32 * sizeof(double);  // dynamic shared memory of k_svd2_lean
 struct LeanGlobal {
   unsigned next_chunk;
   unsigned mode;  // 1: the batch goes to k_svd2_fast
 };
 struct LeanShared {
-  u64 slot2[kRing2];
-  u64 slot0[kRing0];
-  unsigned slot1[kRing1];
-  unsigned tail[3];   // reserved positions per class (free-running)
-  unsigned head1;     // class 1 positions already run (changes inside phases only)
-  unsigned phase;     // != 0: class 1 entries the block is to run now
-  unsigned done;      // warps out of tiles
-  unsigned finished;  // the block's last warp has run the remainders
+  u64 slotT[kRingT];
+  u64 slotS[kRingS];
+  unsigned tail[2];  // reserved positions (free-running): [0] class S, [1] class T
+  unsigned done;     // warps out of tiles
 };
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
-               "l"(gmem)
-               : "memory");
+// The staging buffers (dynamic shared memory: two tiles of 4 x 32 doubles per warp) are addressed as 32-bit
+// shared-memory addresses recomputed from %tid on every tile: a pointer kept across the tile loop gets spilled
+// around the class calls, and its reload queues behind the tile's cp.async copies (12% of all stall samples).
+__device__ __forceinline__ unsigned lean_stage(const void* dyn, unsigned buf) {
+  unsigned tid;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));  // (volatile: not hoisted out of the loop)
+  return static_cast<unsigned>(__cvta_generic_to_shared(dyn)) + (tid >> 5) * 2048u + buf * 1024u + (tid & 31u) * 8u;
 }
-__device__ __forceinline__ void lean_fetch(double (*st)[32], const InP<double>& in, unsigned i, unsigned n32,
-                                           unsigned lane) {
+__device__ __forceinline__ void lean_fetch(unsigned st, const InP<double>& in, unsigned i, unsigned n32) {
   if (i < n32) {
-    cp_async8(&st[0][lane], in.g11 + i);
-    cp_async8(&st[1][lane], in.g12 + i);
-    cp_async8(&st[2][lane], in.g21 + i);
-    cp_async8(&st[3][lane], in.g22 + i);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(st), "l"(in.g11 + i) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(st + 256u), "l"(in.g12 + i) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(st + 512u), "l"(in.g21 + i) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(st + 768u), "l"(in.g22 + i) : "memory");
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ double lds_f64(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
 // The class routes are out-of-line calls: inlined, their register demand pushed
-// the tile loop's own state (tile counters, queue positions) into local memory
-// for the whole loop — a tenth of the kernel's stall samples were reloads of
-// those words.  The batch pointers travel through shared memory (an ABI call
-// would pass fourteen pointers in registers).
+// the tile loop's own state into local memory for the whole loop.  The batch
+// pointers travel through shared memory (an ABI call would pass fourteen
+// pointers in registers).
 struct LeanParams {
   InP<double> in;
   OutP<double> out;
@@ -308,46 +317,31 @@ template <int CLS>
 __device__ __noinline__ void fast_call(const LeanParams* P, unsigned i, unsigned lane) {
   fast_one<double, CLS>(P->in, P->out, i, P->list, P->count, lane);
 }
-// run the queued indices [pos, pos + cnt) of the class 2 or class 0 ring, cnt <= 32
-template <int CLS>
+// run the queued indices [pos, pos + cnt) of a ring, cnt <= 32 (T: class T, else class S)
+template <bool T>
 __device__ __forceinline__ void lean_batch(LeanShared& S, unsigned pos, unsigned cnt, const LeanParams* P,
                                            unsigned lane) {
-  constexpr unsigned ring = CLS == 2 ? kRing2 : kRing0;
-  u64* slots = CLS == 2 ? S.slot2 : S.slot0;
+  constexpr unsigned ring = T ? kRingT : kRingS;
+  u64* slots = T ? S.slotT : S.slotS;
   if (lane < cnt) {
     const unsigned p = pos + lane;
-    const unsigned i = q_take(&slots[p & (ring - 1u)], p / ring, 1u + CLS);
+    const unsigned i = q_take(&slots[p & (ring - 1u)], p / ring, T ? 1u : 2u);
     __threadfence_block();
-    fast_call<CLS>(P, i, lane);
+    fast_call<T ? 3 : 0>(P, i, lane);
   }
   __syncwarp();
-}
-// the block runs S.phase queued class 1 indices, 32 per warp and round (every warp of the block calls this)
-__device__ __forceinline__ void lean_phase1(LeanShared& S, const LeanParams* P, unsigned lane, unsigned wib) {
-  __syncthreads();  // every warp's class 1 entries are in place
-  const unsigned cnt = S.phase, h = S.head1;
-#pragma unroll 1
-  for (unsigned k = 32u * wib + lane; k < cnt; k += 32u * kLeanWarps)
-    fast_call<1>(P, S.slot1[(h + k) & (kRing1 - 1u)], lane);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    S.head1 = h + cnt;
-    S.phase = S.tail[1] - (h + cnt) >= kPhase1 ? kPhase1 : 0u;
-  }
-  __syncthreads();
 }
 __global__ void __launch_bounds__(KOG2_LEAN_THREADS, KOG2_LEAN_MINB)
     k_svd2_lean(InP<double> in, OutP<double> out, uint64_t n, uint32_t* list, unsigned* count, LeanGlobal* G) {
   __shared__ LeanShared S;
   __shared__ LeanParams SP;
   extern __shared__ __align__(16) unsigned char lean_dyn[];  // the input staging buffers (kLeanStageBytes)
-  double(*stage)[2][4][32] = reinterpret_cast<double(*)[2][4][32]>(lean_dyn);
   for (unsigned k = threadIdx.x; k < sizeof(LeanShared) / sizeof(unsigned); k += blockDim.x)
     reinterpret_cast<unsigned*>(&S)[k] = 0u;
   if (threadIdx.x == 0) SP = LeanParams{in, out, list, count};
-  const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  const unsigned lane = threadIdx.x & 31u;
   const unsigned n32 = static_cast<unsigned>(n);
-  // the sample: every block reads the same 512 matrices spread over the batch
+  // the sample: every block reads the same KOG2_LEAN_THREADS matrices spread over the batch
   {
     const uint64_t si = (static_cast<uint64_t>(2u * threadIdx.x + 1u) * n) / (2u * KOG2_LEAN_THREADS);
     const Mat<double> g{in.g11[si], in.g12[si], in.g21[si], in.g22[si]};
@@ -365,21 +359,17 @@ __global__ void __launch_bounds__(KOG2_LEAN_THREADS, KOG2_LEAN_MINB)
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_kog2_lean_total, 1ull);
   }
   // Tiles are handed out eight consecutive tiles (a chunk) at a time from a global counter: warps that run
-  // more batches take fewer chunks (static striding measured 6% slower).  The tile loop carries `base` and
-  // `direct` only — the tile's place in its chunk, its staging buffer and the probe turns follow from base
-  // (chunks start at multiples of 256 matrices), and the next chunk is claimed when it is needed (the round
-  // trip, once per eight tiles, hides behind the other warps): loop words that the compiler has to keep in
-  // local memory around the class calls cost reloads on every tile.
-  // (`direct`, warp-uniform: skip the lean attempt, rides in bit 0 of the loop word — bases are multiples of 32)
+  // more batches take fewer chunks (static striding measured 6% slower).  The tile loop carries ONE word —
+  // the tile base with `direct` (warp-uniform: stop trying svd2_lean) in bit 0; the tile's place in its chunk,
+  // its staging buffer and the probe turns follow from the base (chunks start at multiples of 256 matrices),
+  // and the next chunk is claimed when it is needed (the round trip, once per eight tiles, hides behind the
+  // other warps): loop words that the compiler keeps in local memory around the class calls cost reloads on
+  // every tile (one such reload, queued behind the tile's cp.async copies, was 12.6% of all stall samples).
   unsigned bd = 0;
   if (lane == 0) bd = atomicAdd(&G->next_chunk, 1u);
   bd = __shfl_sync(0xffffffffu, bd, 0) * (kLeanChunk * 32u);
-  lean_fetch(stage[wib][0], in, bd + lane, n32, lane);
+  lean_fetch(lean_stage(lean_dyn, 0u), in, bd + lane, n32);
   while ((bd & ~31u) < n32) {
-    if (ld_vol(&S.phase) != 0u) {  // (warp-uniform: one shared word)
-      lean_phase1(S, &SP, lane, threadIdx.x >> 5);
-      continue;
-    }
     const unsigned base = bd & ~31u;
     bool direct = (bd & 1u) != 0u;
     const unsigned tk = base >> 5;  // tile number: its low bits are the place in the chunk
@@ -390,19 +380,17 @@ __global__ void __launch_bounds__(KOG2_LEAN_THREADS, KOG2_LEAN_MINB)
       nbase = __shfl_sync(0xffffffffu, c, 0) * (kLeanChunk * 32u);  // < 2^32: n <= 2^31, a few chunks per warp beyond
     }
     const unsigned stg = tk & 1u;  // staging buffers alternate (chunks hold an even number of tiles)
-    if (nbase < n32) lean_fetch(stage[wib][stg ^ 1u], in, nbase + lane, n32, lane);
+    if (nbase < n32) lean_fetch(lean_stage(lean_dyn, stg ^ 1u), in, nbase + lane, n32);
     else asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     const unsigned i = base + lane;
     const bool probe = (tk % KOG2_LEAN_PROBE) == 0;
     bool hard = i < n32;
-    unsigned cls = 2;
+    bool simple = false;
     if (hard) {
-      double(*sg)[32] = stage[wib][stg];
-      const Mat<double> g{sg[0][lane], sg[1][lane], sg[2][lane], sg[3][lane]};
-      const unsigned t = type_of(g);
-      // s_type = 0 patterns: 0; t = 15 and one nonzero row or column: 2; else (t ~ 13): 1
-      cls = ((0x0357u >> t) & 1u) ? 0u : (((0x9428u >> t) & 1u) ? 2u : 1u);
+      const unsigned sg = lean_stage(lean_dyn, stg);
+      const Mat<double> g{lds_f64(sg), lds_f64(sg + 256u), lds_f64(sg + 512u), lds_f64(sg + 768u)};
+      simple = ((0x0357u >> type_of(g)) & 1u) != 0u;  // s_type = 0 patterns (classify.hpp:37-42)
       Result<double> r;
       if (!direct || probe) {
         hard = !fast::svd2_lean(g, r);
@@ -419,73 +407,40 @@ __global__ void __launch_bounds__(KOG2_LEAN_THREADS, KOG2_LEAN_MINB)
     if (probe) direct = __popc(mh) > 20;  // svd2_lean pays below ~2/3 of the lanes failing
     bd = nbase | (direct ? 1u : 0u);
     if (mh == 0u) continue;
-    const unsigned m0 = __ballot_sync(0xffffffffu, hard && cls == 0u);
-    const unsigned m1 = __ballot_sync(0xffffffffu, hard && cls == 1u);
-    const unsigned m2 = mh & ~(m0 | m1);
-    // lanes 0..2 reserve their class's positions.  Classes 0 and 2: a
-    // reservation that crosses a multiple of 32 makes this warp run the 32
-    // that end there.  Class 1: the reservation that takes the queue to 512
-    // calls the block to a phase.
+    const unsigned ms = __ballot_sync(0xffffffffu, hard && simple);
+    const unsigned mt = mh & ~ms;
+    // lanes 0 and 1 reserve the positions of classes S and T; a reservation that crosses a multiple of 32
+    // makes this warp run the 32 that end there
     unsigned at = 0, end = 0;
-    bool cross = false;
-    if (lane < 3u) {
-      const unsigned cnt = __popc(lane == 0u ? m0 : (lane == 1u ? m1 : m2));
+    if (lane < 2u) {
+      const unsigned cnt = __popc(lane == 0u ? ms : mt);
       if (cnt != 0u) at = atomicAdd(&S.tail[lane], cnt);
       end = at + cnt;
-      if (lane == 1u) {
-        const unsigned h = ld_vol(&S.head1);
-        if (end - h >= kPhase1 && at - h < kPhase1) *reinterpret_cast<volatile unsigned*>(&S.phase) = kPhase1;
-      } else {
-        cross = (end >> 5) != (at >> 5);
-      }
     }
-    const unsigned run = __ballot_sync(0xffffffffu, cross);
-    const unsigned p0 = (__shfl_sync(0xffffffffu, end, 0) & ~31u) - 32u;
-    const unsigned p2 = (__shfl_sync(0xffffffffu, end, 2) & ~31u) - 32u;
-    at = __shfl_sync(0xffffffffu, at, cls);
+    const unsigned run = __ballot_sync(0xffffffffu, (end >> 5) != (at >> 5));
+    const unsigned ps = (__shfl_sync(0xffffffffu, end, 0) & ~31u) - 32u;
+    const unsigned pt = (__shfl_sync(0xffffffffu, end, 1) & ~31u) - 32u;
+    at = __shfl_sync(0xffffffffu, at, simple ? 0 : 1);
     if (hard) {
-      const unsigned mine = cls == 0u ? m0 : (cls == 1u ? m1 : m2);
-      const unsigned at1 = at + __popc(mine & ((1u << lane) - 1u));
-      if (cls == 1u) {
-        S.slot1[at1 & (kRing1 - 1u)] = i;  // never full: a phase starts at 512 and every warp joins within a tile
-      } else {
-        // one wait loop for the two ring classes (each lane its own slot)
-        u64* slot = cls == 2u ? &S.slot2[at1 & (kRing2 - 1u)] : &S.slot0[at1 & (kRing0 - 1u)];
-        q_put(slot, cls == 2u ? at1 / kRing2 : at1 / kRing0, i, 8u + cls);
-      }
+      const unsigned at1 = at + __popc((simple ? ms : mt) & ((1u << lane) - 1u));
+      // one wait loop for the two rings (each lane its own slot)
+      u64* slot = simple ? &S.slotS[at1 & (kRingS - 1u)] : &S.slotT[at1 & (kRingT - 1u)];
+      q_put(slot, simple ? at1 / kRingS : at1 / kRingT, i, 8u);
     }
     __syncwarp();
-    if (run & 4u) lean_batch<2>(S, p2, 32u, &SP, lane);
-    if (run & 1u) lean_batch<0>(S, p0, 32u, &SP, lane);
+    if (run & 2u) lean_batch<true>(S, pt, 32u, &SP, lane);
+    if (run & 1u) lean_batch<false>(S, ps, 32u, &SP, lane);
   }
-  // out of tiles
+  // out of tiles: the block's last warp runs the remainders of the two rings (< 32 each) as partial batches
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __threadfence_block();
   unsigned l = 0;
   if (lane == 0) l = atomicAdd(&S.done, 1u) == kLeanWarps - 1u;
-  if (!__shfl_sync(0xffffffffu, l, 0)) {  // stand by for phases until the block's last warp is through
-    while (ld_vol(&S.finished) == 0u) {
-      if (ld_vol(&S.phase) != 0u) lean_phase1(S, &SP, lane, threadIdx.x >> 5);
-      else __nanosleep(500);
-    }
-    return;
-  }
-  // the block's last warp: every other warp has run its batches and stands by.  What is left of class 1
-  // runs as more phases, then the remainders of the two rings (< 32 each) as partial batches.
+  if (!__shfl_sync(0xffffffffu, l, 0)) return;
   __threadfence_block();
-  for (;;) {
-    if (ld_vol(&S.phase) == 0u) {
-      const unsigned r1 = ld_vol(&S.tail[1]) - ld_vol(&S.head1);
-      if (r1 == 0u) break;
-      *reinterpret_cast<volatile unsigned*>(&S.phase) = r1 < kPhase1 ? r1 : kPhase1;
-    }
-    lean_phase1(S, &SP, lane, threadIdx.x >> 5);
-  }
-  const unsigned t2 = ld_vol(&S.tail[2]), t0 = ld_vol(&S.tail[0]);
-  if (t2 & 31u) lean_batch<2>(S, t2 & ~31u, t2 & 31u, &SP, lane);
-  if (t0 & 31u) lean_batch<0>(S, t0 & ~31u, t0 & 31u, &SP, lane);
-  __threadfence_block();
-  if (lane == 0) *reinterpret_cast<volatile unsigned*>(&S.finished) = 1u;
+  const unsigned tt = ld_vol(&S.tail[1]), ts = ld_vol(&S.tail[0]);
+  if (tt & 31u) lean_batch<true>(S, tt & ~31u, tt & 31u, &SP, lane);
+  if (ts & 31u) lean_batch<false>(S, ts & ~31u, ts & 31u, &SP, lane);
 }
 // k_svd2_fast for a batch whose sample sent it back (LeanGlobal::mode)
 #ifdef KOG2_FAST_TMA
