@@ -391,16 +391,20 @@ __global__ void __launch_bounds__(KOG2_LEAN_THREADS, KOG2_LEAN_MINB)
       const unsigned sg = lean_stage(lean_dyn, stg);
       const Mat<double> g{lds_f64(sg), lds_f64(sg + 256u), lds_f64(sg + 512u), lds_f64(sg + 768u)};
       simple = ((0x0357u >> type_of(g)) & 1u) != 0u;  // s_type = 0 patterns (classify.hpp:37-42)
-      Result<double> r;
+      // (queued lanes store too: whole sectors at the first touch.  Two store sites rather than one behind a
+      // merged Result: the merge cost twenty register moves per tile.)
       if (!direct || probe) {
+        Result<double> r;
         hard = !fast::svd2_lean(g, r);
+        store_result<false>(out, i, r);
       } else {
+        Result<double> r;
         r.u = r.v = g;
         r.sigma1 = r.sigma2 = EPair<double>{0, 0.0};
         r.s = 0;
         r.flags = 0;
+        store_result<false>(out, i, r);
       }
-      store_result<false>(out, i, r);  // queued lanes too: whole sectors at the first touch
       asm volatile("fence.acq_rel.cta;" ::: "memory");  // before the push (lighter than __threadfence_block's fence.sc)
     }
     const unsigned mh = __ballot_sync(0xffffffffu, hard);
