@@ -231,6 +231,8 @@ def load(path: str | None = None) -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if os.environ.get("KOG2_LEAN_MIN_LOG2"):  # tuning runs (tools/lean_sizes.sh): the two-speed kernel's threshold
+        lib.kog_svd2_set_lean_min(1 << int(os.environ["KOG2_LEAN_MIN_LOG2"]))
     if path is None:
         _lib = lib
     return lib

@@ -558,9 +558,9 @@ __global__ void __launch_bounds__(kThreads, 3)
 
 constexpr uint64_t kFastChunk = 1ull << 31;  // uint32 deferred indices per launch pair
 // smaller batches: k_svd2_fast alone — the two-speed kernel's start (sample, queue set-up) and end (partial
-// batches, the blocks' last phases) cost ~50 us; it breaks even near 2^23.5 config-3 matrices
-// (profiles/r3_lean_sizes.txt).  kog_svd2_set_lean_min moves the threshold (tests run the kernel on less).
-static std::atomic<uint64_t> g_lean_min{1ull << 24};
+// batches) cost ~30 us; it ties at 2^21 config-3 matrices and is 14% ahead at 2^22
+// (profiles/r3_lean_sizes.txt).  kog_svd2_set_lean_min moves the threshold.
+static std::atomic<uint64_t> g_lean_min{1ull << 22};
 
 template <class T, class MatC, class OutC>
 int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* opt, cudaStream_t st) {
