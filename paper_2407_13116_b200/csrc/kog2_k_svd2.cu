@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(KOG2_LEAN_THREADS, KOG2_LEAN_MINB)
       nbase = __shfl_sync(0xffffffffu, c, 0) * (kLeanChunk * 32u);  // < 2^32: n <= 2^31, a few chunks per warp beyond
     }
     const unsigned stg = tk & 1u;  // staging buffers alternate (chunks hold an even number of tiles)
-    if (nbase < n32) lean_fetch(lean_stage(lean_dyn, stg ^ 1u), in, nbase + lane, n32);
+    const unsigned sg = lean_stage(lean_dyn, stg);  // this tile's buffer; the other one is 1 KB away
+    if (nbase < n32) lean_fetch(sg + 1024u - 2048u * stg, in, nbase + lane, n32);
     else asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     const unsigned i = base + lane;
@@ -388,7 +389,6 @@ __global__ void __launch_bounds__(KOG2_LEAN_THREADS, KOG2_LEAN_MINB)
     bool hard = i < n32;
     bool simple = false;
     if (hard) {
-      const unsigned sg = lean_stage(lean_dyn, stg);
       const Mat<double> g{lds_f64(sg), lds_f64(sg + 256u), lds_f64(sg + 512u), lds_f64(sg + 768u)};
       simple = ((0x0357u >> type_of(g)) & 1u) != 0u;  // s_type = 0 patterns (classify.hpp:37-42)
       // (queued lanes store too: whole sectors at the first touch.  Two store sites rather than one behind a
