@@ -56,7 +56,7 @@ __device__ __forceinline__ bool svd2_lean(const Mat<double>& gi, Result<double>&
   // factor 2 (1 - 2^-20) or more), so comparing the larger entries decides w1 < w2 as the norms would.
   const bool near1 = abs(d1) < (28 << 20), near2 = abs(d2) < (28 << 20);
   const int m1 = max(h11, h21), m2 = max(h12, h22);
-  bad |= (near1 && (near2 || m2 - m1 < (1 << 20))) || (near2 && m1 - m2 < (1 << 20));
+  bad |= (near1 & (near2 | (m2 - m1 < (1 << 20)))) | (near2 & (m1 - m2 < (1 << 20)));  // (no short circuits: no branches)
   const bool lo1 = d1 < 0, lo2 = d2 < 0;  // the column's larger entry sits in row 1
   const bool col_swap = fabs(lo1 ? gi.g21 : gi.g11) < fabs(lo2 ? gi.g22 : gi.g12);
   // the pivot column (cx, cy) and the other one (ox, oy); row signs make the
