@@ -33,6 +33,8 @@
 namespace kog2 {
 namespace fast {
 
+// -x on the integer pipe (the compiler's DADD -RZ, -x takes an FP64 issue slot)
+__device__ __forceinline__ double neg_i(double x) { return sethi(x, hiw(x) ^ static_cast<int>(0x80000000u)); }
 __device__ __forceinline__ bool below_2m27(double x) {  // 0 <= x < 2^-27 on a non-negative finite x
   return hiw(x) < 0x3e400000;
 }
@@ -82,7 +84,7 @@ __device__ __forceinline__ bool svd2_lean(const Mat<double>& gi, Result<double>&
   // wide_dot2_div (svd2.hpp:281-321) of (A a11 + C a21) / a11 / 1, as wide_n
   double we;
   {
-    const double A = same ? a22 : a12, C = same ? -a12 : a22;
+    const double A = same ? a22 : a12, C = same ? neg_i(a12) : a22;
     const int la = bexp(hiw(A)), lb = bexp(hiw(a11)), lc = bexp(hiw(C)), ld = bexp(hiw(a21));  // biased
     const int sa = la + lb, sb = lc + ld;
     const int scale = max(sa, sb);
@@ -140,13 +142,13 @@ __device__ __forceinline__ bool svd2_lean(const Mat<double>& gi, Result<double>&
   const int hcn = hiw(cnum) & 0x7fffffff;
   bad |= cden != 1.0 || static_cast<unsigned>(hcn - 0x00100000) >= static_cast<unsigned>(0x3e400000 - 0x00100000);
   const double sn = cnum;  // tan(chi) / 1
-  Mat<double> m{1.0, -sn, sn, 1.0};
-  if (minus) m = Mat<double>{m.g11, m.g12, -m.g21, -m.g22};
+  Mat<double> m{1.0, neg_i(sn), sn, 1.0};
+  if (minus) m = Mat<double>{m.g11, m.g12, neg_i(m.g21), neg_i(m.g22)};
   if (row_swap) m = Mat<double>{m.g21, m.g22, m.g11, m.g12};
   out.u = Mat<double>{sgnmul(sr0, m.g11), sgnmul(sr0, m.g12), sgnmul(sr1, m.g21), sgnmul(sr1, m.g22)};
   const int s12 = hiw(r12_raw) >> 31 | 1;
   const SP vplus = sp_mul(col_swap ? sp_exchange() : sp_identity(), sp_row_signs(1, s12));
-  out.v = apply_left(vplus, Mat<double>{1.0, -tpsi, tpsi, 1.0});
+  out.v = apply_left(vplus, Mat<double>{1.0, neg_i(tpsi), tpsi, 1.0});
   out.sigma1 = EPair<double>{bexp(hr11) - 1023 - s, mant_n(r11)};
   out.sigma2 = EPair<double>{p22.e - s, p22.f};
   out.s = s;
