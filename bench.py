@@ -336,7 +336,7 @@ SHAPE_OF = {1: "general (circ)", 2: "upper-triangular (e in [-1000,1000])", 3: "
 
 def kernels_of(suf: str, n: int) -> str:
     """the launches behind one kog_svd2_batch call (csrc/kog2_k_svd2.cu: launch_svd2)"""
-    if suf == "f64" and n >= 1 << 22:
+    if suf == "f64" and n >= 1 << 23:
         return ("k_svd2_lean (two-speed kernel; hands the batch back to the k_svd2_fast launched behind it if "
                 "its input sample says so) + k_svd2_list (one kog_svd2_batch_f64 call)")
     return f"k_svd2_fast + k_svd2_list (one kog_svd2_batch_{suf} call)"

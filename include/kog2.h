@@ -428,13 +428,13 @@ int kog_div_batch_f32(const float* x, const float* y, float* out, uint64_t n, vo
  * current device since the library was loaded (synchronous; -1 on error).
  * Diagnostics only: take differences around the calls of interest. */
 int64_t kog_svd2_deferred_count(void);
-/* kog_svd2_batch_f64 launches (default Options, batches of 2^22 matrices and more) whose
+/* kog_svd2_batch_f64 launches (default Options, batches of 2^23 matrices and more) whose
  * input sample kept them on the two-speed kernel (k_svd2_lean) instead of
  * handing the batch back to k_svd2_fast, on the current device since load
  * (synchronous; -1 on error).  Diagnostics only. */
 int64_t kog_svd2_lean_count(void);
 /* Tuning knob: the smallest kog_svd2_batch_f64 batch (default Options) that is
- * offered to the two-speed kernel (default 2^22; at least 2^16).  Returns the
+ * offered to the two-speed kernel (default 2^23; at least 2^16).  Returns the
  * previous value.  Results do not depend on it. */
 uint64_t kog_svd2_set_lean_min(uint64_t n);
 /* number of kernel launches issued by this library since load */

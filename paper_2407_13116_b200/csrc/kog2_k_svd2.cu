@@ -557,10 +557,11 @@ __global__ void __launch_bounds__(kThreads, 3)
 }
 
 constexpr uint64_t kFastChunk = 1ull << 31;  // uint32 deferred indices per launch pair
-// smaller batches: k_svd2_fast alone — the two-speed kernel's start (sample, queue set-up) and end (partial
-// batches) cost ~30 us; it ties at 2^21 config-3 matrices and is 14% ahead at 2^22
-// (profiles/r3_lean_sizes.txt).  kog_svd2_set_lean_min moves the threshold.
-static std::atomic<uint64_t> g_lean_min{1ull << 22};
+// smaller batches: k_svd2_fast alone.  The two-speed kernel's start (sample, queue set-up) and end (partial
+// batches) cost ~30 us: it ties at 2^21 config-3 matrices and is 14% ahead at 2^22 (profiles/r3_lean_sizes.txt),
+// but the host pipeline's 2^22-matrix chunks ran 3% slower end to end on it (its extra stream operations per
+// chunk; the pipeline is PCIe-bound either way), so the threshold sits above them.  kog_svd2_set_lean_min moves it.
+static std::atomic<uint64_t> g_lean_min{1ull << 23};
 
 template <class T, class MatC, class OutC>
 int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* opt, cudaStream_t st) {
@@ -619,9 +620,16 @@ int launch_svd2(const MatC* in, const OutC* out, uint64_t n, const kog_options* 
                 rc = kog2_cuda_error("cudaMemsetAsync(lean queues)");
                 break;
               }
-              // (per device, so on every launch: microseconds against a kernel of a millisecond and more)
-              const bool smem_ok = cudaFuncSetAttribute(k_svd2_lean, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                        static_cast<int>(kLeanStageBytes)) == cudaSuccess;
+              // (function attributes are per device: once per device, not once per process)
+              static std::atomic<bool> attr_set[64];
+              int dev = 0;
+              cudaGetDevice(&dev);
+              bool smem_ok = dev >= 0 && dev < 64 && attr_set[dev].load(std::memory_order_acquire);
+              if (!smem_ok) {
+                smem_ok = cudaFuncSetAttribute(k_svd2_lean, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(kLeanStageBytes)) == cudaSuccess;
+                if (smem_ok && dev >= 0 && dev < 64) attr_set[dev].store(true, std::memory_order_release);
+              }
               if (!smem_ok) {
                 rc = kog2_cuda_error("cudaFuncSetAttribute(k_svd2_lean)");
                 break;
