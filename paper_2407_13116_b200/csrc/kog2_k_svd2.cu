@@ -239,16 +239,6 @@ __device__ __forceinline__ unsigned q_take(u64* slot, unsigned lap, unsigned sit
   *vs = q_word(2u * lap + 2u, 0u);
   return static_cast<unsigned>(w);
 }
-// Block shape: one block of 1024 threads per SM.  Thirty-two warps on one set of queues fill a batch twice as
-// fast as sixteen (the queued matrices' sectors are younger in L2) and the SM holds one hot code set instead of
-// two blocks' worth.  Measured (config 3, ms per 2^28, class 1 phase = 32 per warp): 256 x 4: 10.65,
-// 512 x 2: 10.51, 1024 x 1: 10.04 (phase 512: 10.57, 2048: 10.17).
-#ifndef KOG2_LEAN_THREADS
-#define KOG2_LEAN_THREADS 1024
-#endif
-#ifndef KOG2_LEAN_MINB
-#define KOG2_LEAN_MINB 1
-#endif
 // launches the sample kept on this kernel (diagnostics: kog_svd2_lean_count)
 __device__ unsigned long long g_kog2_lean_total = 0;
 // Block shape: one block of 1024 threads per SM.  Thirty-two warps on one set of queues fill a batch twice as
