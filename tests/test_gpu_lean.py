@@ -136,3 +136,82 @@ def test_lean_kernel_guard_zones(cuda, ref):
     A.check("k_svd2_lean")
     assert lib.kog_svd2_lean_count() == kept0 + 1
     compare_svd(outs, refbind.svd2(ref, g), "guarded two-speed call")
+
+
+def _edge_matrices(rng: np.random.Generator, reps: int) -> np.ndarray:
+    """matrices that sit on svd2_lean's acceptance thresholds (kog2_lean.cuh):
+    column entries 28 binades apart give or take a binade and an ulp of the
+    high word, a near column whose larger entry is half the other column's
+    give or take the same, r12 against r11 and tan(2 phi) around 2^-27 — each
+    with random significands, signs and row/column arrangements"""
+    out = []
+
+    def rnd_m(k):  # significands in [1, 2), some at the ends of the range
+        m = 1.0 + rng.random(k)
+        pick = rng.integers(0, 8, k)
+        m[pick == 0] = 1.0
+        m[pick == 1] = np.nextafter(2.0, 1.0)
+        m[pick == 2] = 1.0 + 2.0 ** -20
+        m[pick == 3] = 1.0 + 2.0 ** -20 - 2.0 ** -52
+        return m
+
+    def emit(g11, g12, g21, g22):
+        g = np.stack([g11, g12, g21, g22])
+        k = g.shape[1]
+        g = g * rng.choice([-1.0, 1.0], size=(4, k))
+        # random row and column exchanges (rows: g11<->g21, g12<->g22; columns: g11<->g12, g21<->g22)
+        rs, cs = rng.random(k) < 0.5, rng.random(k) < 0.5
+        g[:, rs] = g[[2, 3, 0, 1]][:, rs]
+        g[:, cs] = g[[1, 0, 3, 2]][:, cs]
+        out.append(g)
+
+    for _ in range(reps):
+        k = 4096
+        E = rng.integers(-300, 300, k).astype(np.float64)
+        # 1. the pivot column's gap around 28 binades; the other column far below and separated
+        d = rng.choice([26, 27, 28, 29, 30], k).astype(np.float64)
+        x = rnd_m(k) * 2.0 ** E
+        y = rnd_m(k) * 2.0 ** (E - d)
+        p = rnd_m(k) * 2.0 ** (E - rng.integers(40, 200, k))
+        q = rnd_m(k) * 2.0 ** (E - rng.integers(240, 400, k))
+        emit(x, p, y, q)
+        # 2. a near column (entries within a few binades) beside a separated one whose larger entry is about
+        #    twice the near column's: the exchange decided with or without the norm
+        a = rnd_m(k) * 2.0 ** E
+        a2 = a * rng.choice([1.0, 0.9, 0.5, 0.75, 2.0 ** -5, 2.0 ** -27], k)
+        ratio = rng.choice([1.0, 2.0 ** 0.5, 1.9999990463256836, 2.0, 2.0000019073486328, 4.0, 2.0 ** -1, 2.0 ** 20], k)
+        b = np.maximum(np.abs(a), np.abs(a2)) * ratio * rng.choice([1.0, np.nextafter(1.0, 0.0), np.nextafter(1.0, 2.0)], k)
+        b2 = b * 2.0 ** -rng.integers(29, 90, k).astype(np.float64) * rnd_m(k)
+        emit(a, b, a2, b2)
+        # 3. r12 against r11 around 2^-27 .. 2^-29 (tan psi and the hypot(r11, r12) early-out), r22 anywhere below
+        x = rnd_m(k) * 2.0 ** E
+        y = rnd_m(k) * 2.0 ** (E - rng.choice([26, 27, 28, 29], k))
+        z = rnd_m(k) * 2.0 ** (E - rng.integers(0, 120, k))
+        tiny = x * 2.0 ** -rng.integers(60, 300, k).astype(np.float64)
+        emit(x, y, tiny, z)
+        # 4. tan(2 phi) = 2 r12 r22 / (r11^2 - r22^2) around 2^-27
+        x = rnd_m(k) * 2.0 ** E
+        e12 = rng.integers(0, 28, k)
+        y = rnd_m(k) * 2.0 ** (E - e12 - 29)
+        z = rnd_m(k) * 2.0 ** (E - (28 - e12) + rng.integers(-1, 2, k))
+        emit(x, y, x * 2.0 ** -200.0, np.minimum(z, x * 0.999))
+    return np.ascontiguousarray(np.concatenate(out, axis=1))
+
+
+def test_lean_kernel_threshold_edges(cuda, ref):
+    """svd2_lean's acceptance tests at their thresholds (inside a config-3
+    batch, so that the kernel's sample keeps it): every lane, accepted or
+    queued, equals the reference"""
+    rng = np.random.default_rng(0x1EA4)
+    edges = _edge_matrices(rng, 8)
+    assert np.isfinite(edges).all() and (edges != 0).all()
+    n = 1 << 22
+    g = cfg_host(3, n, 777)
+    pos = rng.permutation(n)[:edges.shape[1]]  # scattered through the batch: every warp meets some
+    g[:, pos] = edges
+    lib = capi.load()
+    kept0 = lib.kog_svd2_lean_count()
+    got = K.svd2(dev(g))
+    torch.cuda.synchronize()
+    assert lib.kog_svd2_lean_count() == kept0 + 1
+    compare_svd(got, refbind.svd2(ref, g), "threshold edges")
