@@ -108,6 +108,93 @@ __device__ __forceinline__ uint32_t run_one_buf(const Mat<T>& g, const SvdBuf<T>
   return flags;
 }
 
+// ------------------------------------------------- the split study
+// k_study's per-matrix body is ~9,000 straight-line instructions (150 KB of SASS executed once per matrix):
+// every warp streams it through a 32 KB instruction cache, and the kernel runs at the rate its leading warp can
+// fetch code (ncu r8: 22% of stall samples `no_instructions`, the GPC instruction cache at 41% of its request
+// peak with a 41% hit rate; with 20 warps per SM instead of 16 the same code ran 3x slower, 80% of samples
+// `no_instructions`).  The phased study therefore runs the body as separate kernels whose loops stay in the
+// instruction cache — the reference singular values, the reconstruction error, one orthogonality defect per
+// launch — and a last kernel that adds the singular values' errors and absorbs; the pieces go through
+// 10 x 8 B per matrix of chunk buffers.  Same operations on the same values: identical statistics.
+struct StudyAux {
+  double *reG, *reU, *reV;
+  uint32_t* fin;  // g, u, v and the computed singular values are finite (metrics()'s Xf route, but for ref)
+};
+
+// the factors as run_one_buf expands them
+template <class T>
+__device__ __forceinline__ Mat<T> factor_of(T q11, T q12, bool neg21, bool neg22) {
+  return Mat<T>{q11, q12, with_sign(fabs(q12), neg21), with_sign(fabs(q11), neg22)};
+}
+
+#ifndef KOG2_SPLIT_MINB
+#define KOG2_SPLIT_MINB 2
+#endif
+// svd2_ext's singular values (ref_sigma: inline Xf where it applies) of a chunk
+template <class T>
+__global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_sigma(InP<T> in, SvdBuf<T> b, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    ExtSvd ref;
+    ref_sigma<T>(load_mat(in, i), ref);
+    b.re1[i] = ref.sigma1.e;
+    b.rh1[i] = ref.sigma1.hi;
+    b.rl1[i] = ref.sigma1.lo;
+    b.re2[i] = ref.sigma2.e;
+    b.rh2[i] = ref.sigma2.hi;
+    b.rl2[i] = ref.sigma2.lo;
+  }
+}
+// reG of the finite lanes, and which lanes those are
+template <class T>
+__global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_recon(InP<T> in, SvdBuf<T> b, StudyAux a, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const Mat<T> g = load_mat(in, i);
+    const uint32_t flags = b.flags[i];
+    const Mat<T> u = factor_of<T>(b.u11[i], b.u12[i], flags & KOG_F_SIGN_U21, flags & KOG_F_SIGN_U22);
+    const Mat<T> v = factor_of<T>(b.v11[i], b.v12[i], flags & KOG_F_SIGN_V21, flags & KOG_F_SIGN_V22);
+    const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
+    const bool fin = mat_finite(g) && mat_finite(u) && mat_finite(v) && is_finite(s1.f) && is_finite(s2.f);
+    a.fin[i] = fin ? 1u : 0u;
+    if (fin) a.reG[i] = xf_recon(g, u, v, xf_of(ext_from_pair(s1)), xf_of(ext_from_pair(s2)));
+  }
+}
+// the orthogonality defect of one factor (launched for U and for V) of the finite lanes
+template <class T>
+__global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB)
+    k_study_ortho(const T* q11, const T* q12, const uint32_t* flags, uint32_t bit21, uint32_t bit22,
+                  const uint32_t* fin, double* out, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    if (!fin[i]) continue;
+    const uint32_t f = flags[i];
+    out[i] = xf_ortho(factor_of<T>(q11[i], q12[i], f & bit21, f & bit22));
+  }
+}
+// run_one on the pieces: the singular values' errors and kappa here; lanes off the Xf route (anything not
+// finite) run metrics() whole on the Ext functions, as in run_one_buf
+template <class T>
+__device__ __forceinline__ uint32_t run_one_split(const InP<T>& gin, const SvdBuf<T>& b, const StudyAux& a, uint64_t i,
+                                                  Metrics& m) {
+  ExtSvd ref;
+  ref.sigma1 = Ext{b.re1[i], b.rh1[i], b.rl1[i]};
+  ref.sigma2 = Ext{b.re2[i], b.rh2[i], b.rl2[i]};
+  uint32_t flags = b.flags[i];
+  const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
+  if (a.fin[i] != 0 && ref_sigma_finite(ref)) {
+    m.reG = a.reG[i];
+    m.reU = a.reU[i];
+    m.reV = a.reV[i];
+    xf_sigma_metrics(xf_of(ext_from_pair(s1)), xf_of(ext_from_pair(s2)), xf_of(ref.sigma1), xf_of(ref.sigma2), m);
+  } else {
+    const Mat<T> u = factor_of<T>(b.u11[i], b.u12[i], flags & KOG_F_SIGN_U21, flags & KOG_F_SIGN_U22);
+    const Mat<T> v = factor_of<T>(b.v11[i], b.v12[i], flags & KOG_F_SIGN_V21, flags & KOG_F_SIGN_V22);
+    if (!all_finite(u) || !all_finite(v) || !is_finite(s1.f) || !is_finite(s2.f)) flags |= KOG_M_NONFINITE_FACTOR;
+    metrics_ext<T>(load_mat(gin, i), u, v, ext_from_pair(s1), ext_from_pair(s2), ref, m);
+  }
+  if (isnan(m.reG) || isnan(m.reS1) || isnan(m.reS2) || isnan(m.reU) || isnan(m.reV)) flags |= KOG_M_NAN_METRIC;
+  return flags;
+}
+
 template <class T>
 __device__ __forceinline__ uint32_t run_one_lasv2(const Mat<T>& g, Metrics& m) {
   ExtSvd ref;
@@ -178,10 +265,10 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 #define KOG2_STUDY_THREADS 256
 #endif
 constexpr int kStudyThreads = KOG2_STUDY_THREADS;
-template <class T, int ROUTINE, bool PHASED>
+template <class T, int ROUTINE, int PHASED>  // PHASED: 0 fused, 1 from the chunk's svd2 buffers, 2 from the split kernels' pieces too
 __global__ void __launch_bounds__(kStudyThreads, KOG2_STUDY_MINB)
     k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt, kog_stats* stats, BlockPartial* partial, InP<T> gin,
-            SvdBuf<T> sb, bool accumulate) {
+            SvdBuf<T> sb, bool accumulate, StudyAux aux) {
   __shared__ unsigned cnt[19];
   __shared__ double red[5][kStudyThreads / 32];
   __shared__ Ext kred_k[kStudyThreads / 32];
@@ -200,7 +287,9 @@ __global__ void __launch_bounds__(kStudyThreads, KOG2_STUDY_MINB)
     const unsigned long long index = index0 + i;
     Metrics m;
     uint32_t flags;
-    if constexpr (PHASED) {  // generated and decomposed by the earlier launches of this chunk
+    if constexpr (PHASED == 2) {
+      flags = run_one_split<T>(gin, sb, aux, i, m);
+    } else if constexpr (PHASED == 1) {  // generated and decomposed by the earlier launches of this chunk
       flags = run_one_buf<T>(load_mat(gin, i), sb, i, m);
     } else {
       const Mat<T> g = generate<T>(c, index);
@@ -423,6 +512,14 @@ int study_streams_mode() {
   }();
   return v;
 }
+// the metrics as separate kernels (default) or inside k_study (KOG2_STUDY_SPLIT=0, for A/B)
+bool study_split() {
+  static const bool v = [] {
+    const char* e = std::getenv("KOG2_STUDY_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 // the phased k_study's blocks per SM (KOG2_STUDY_BPS overrides, for tuning)
 int study_bps() {
   static const int v = [] {
@@ -471,7 +568,9 @@ template <class T>
 int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats, int sms, cudaStream_t st) {
   const uint64_t C = n < kStudyChunk ? n : kStudyChunk;
   const int nbuf = n > C ? 2 : 1;  // two chunk buffers when there is more than one chunk
-  const size_t per = static_cast<size_t>(C) * (6 * 8 + 10 * sizeof(T) + 4 * sizeof(int32_t));
+  // per matrix: the reference singular values (6 x 8 B), reG/reU/reV (3 x 8 B), the input and the compact
+  // decomposition (10 T), exponents and flags (4 x 4 B), the finite-lane marks (4 B)
+  const size_t per = static_cast<size_t>(C) * (9 * 8 + 10 * sizeof(T) + 5 * sizeof(int32_t));
   const int gmax = study_grid(C, sms, study_bps());
   // one set of per-block kappa slots per consumer stream (concurrent k_study
   // launches never share a slot) after the chunk buffers
@@ -510,12 +609,14 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
     typename Abi<T>::Out om;
     InP<T> gin;
     SvdBuf<T> sb;
+    StudyAux aux;
   } bufs[2];
   for (int k = 0; k < nbuf; ++k) {
     double* rd = reinterpret_cast<double*>(ws + per * k);  // the 8-byte arrays first
     long long* rq = reinterpret_cast<long long*>(rd);
-    T* t = reinterpret_cast<T*>(rd + 6 * C);
+    T* t = reinterpret_cast<T*>(rd + 9 * C);
     int32_t* w = reinterpret_cast<int32_t*>(t + 10 * C);
+    bufs[k].aux = StudyAux{rd + 6 * C, rd + 7 * C, rd + 8 * C, reinterpret_cast<uint32_t*>(w + 4 * C)};
     bufs[k].gm = typename Abi<T>::Mat{t, t + C, t + 2 * C, t + 3 * C};
     const typename Abi<T>::Out om{t + 4 * C, t + 5 * C, w,         w + C,     t + 6 * C,
                                   t + 7 * C, t + 8 * C, t + 9 * C, w + 2 * C, reinterpret_cast<uint32_t*>(w + 3 * C)};
@@ -560,8 +661,24 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
     if ((rc = launched("k_ref_sigma")) != KOG_OK) break;
 #endif
     const int grid = study_grid(len, sms, study_bps());
-    k_study<T, KOG_ROUTINE_KOG, true><<<grid, kStudyThreads, 0, q>>>(GenCfg{}, index0 + lo, len, Opt{}, stats,
-                                                                   part + k * gmax, bf.gin, bf.sb, true);
+    if (study_split()) {
+      const int gs = grid_for(len);
+      k_study_sigma<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.sb, len);
+      if ((rc = launched("k_study_sigma")) != KOG_OK) break;
+      k_study_recon<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.sb, bf.aux, len);
+      if ((rc = launched("k_study_recon")) != KOG_OK) break;
+      k_study_ortho<T><<<gs, kThreads, 0, q>>>(bf.sb.u11, bf.sb.u12, bf.sb.flags, KOG_F_SIGN_U21, KOG_F_SIGN_U22,
+                                               bf.aux.fin, bf.aux.reU, len);
+      if ((rc = launched("k_study_ortho")) != KOG_OK) break;
+      k_study_ortho<T><<<gs, kThreads, 0, q>>>(bf.sb.v11, bf.sb.v12, bf.sb.flags, KOG_F_SIGN_V21, KOG_F_SIGN_V22,
+                                               bf.aux.fin, bf.aux.reV, len);
+      if ((rc = launched("k_study_ortho")) != KOG_OK) break;
+      k_study<T, KOG_ROUTINE_KOG, 2><<<grid, kStudyThreads, 0, q>>>(GenCfg{}, index0 + lo, len, Opt{}, stats,
+                                                                    part + k * gmax, bf.gin, bf.sb, true, bf.aux);
+    } else {
+      k_study<T, KOG_ROUTINE_KOG, 1><<<grid, kStudyThreads, 0, q>>>(GenCfg{}, index0 + lo, len, Opt{}, stats,
+                                                                    part + k * gmax, bf.gin, bf.sb, true, StudyAux{});
+    }
     if ((rc = launched("k_study")) != KOG_OK) break;
     if (cudaEventRecord(freed[k], q) != cudaSuccess) {
       rc = kog2_cuda_error("study chunk release");
@@ -633,10 +750,10 @@ int kog_study_batch(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_
   const Opt o = opt_of(&cfg->options);
   if (cfg->single_precision)
     k_study<float, KOG_ROUTINE_LASV2, false><<<grid, kStudyThreads, 0, st>>>(gen_cfg_of<float>(cfg), index0, n, o, stats_dev,
-                                                                         part, InP<float>{}, SvdBuf<float>{}, false);
+                                                                         part, InP<float>{}, SvdBuf<float>{}, false, StudyAux{});
   else
     k_study<double, KOG_ROUTINE_LASV2, false><<<grid, kStudyThreads, 0, st>>>(gen_cfg_of<double>(cfg), index0, n, o, stats_dev,
-                                                                          part, InP<double>{}, SvdBuf<double>{}, false);
+                                                                          part, InP<double>{}, SvdBuf<double>{}, false, StudyAux{});
   int rc = launched("k_study");
   if (rc == KOG_OK) {
     k_study_finish<<<1, kThreads, 0, st>>>(stats_dev, part, grid);
