@@ -118,8 +118,10 @@ __device__ __forceinline__ uint32_t run_one_buf(const Mat<T>& g, const SvdBuf<T>
 // launch — and a last kernel that adds the singular values' errors and absorbs; the pieces go through
 // 10 x 8 B per matrix of chunk buffers.  Same operations on the same values: identical statistics.
 struct StudyAux {
-  double *reG, *reU, *reV;
-  uint32_t* fin;  // g, u, v and the computed singular values are finite (metrics()'s Xf route, but for ref)
+  double *reG, *reU, *reV, *reS1, *reS2, *kh, *kl;  // kappa_2 = (ke, kh, kl)
+  int32_t* ke;
+  uint32_t* sflag;  // bit 0: the reference singular values are finite; bit 1: kappa_inf
+  uint32_t* fin;    // g, u, v and the computed singular values are finite (with bit 0 above: metrics()'s Xf route)
 };
 
 // the factors as run_one_buf expands them
@@ -133,16 +135,24 @@ __device__ __forceinline__ Mat<T> factor_of(T q11, T q12, bool neg21, bool neg22
 #endif
 // svd2_ext's singular values (ref_sigma: inline Xf where it applies) of a chunk
 template <class T>
-__global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_sigma(InP<T> in, SvdBuf<T> b, uint64_t n) {
+__global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_sigma(InP<T> in, SvdBuf<T> b, StudyAux a, uint64_t n) {
   for (uint64_t i = gtid(); i < n; i += gstride()) {
     ExtSvd ref;
     ref_sigma<T>(load_mat(in, i), ref);
-    b.re1[i] = ref.sigma1.e;
-    b.rh1[i] = ref.sigma1.hi;
-    b.rl1[i] = ref.sigma1.lo;
-    b.re2[i] = ref.sigma2.e;
-    b.rh2[i] = ref.sigma2.hi;
-    b.rl2[i] = ref.sigma2.lo;
+    const bool rf = ref_sigma_finite(ref);
+    uint32_t sf = rf ? 1u : 0u;
+    if (rf) {  // the singular values' errors and kappa_2 (used by the lanes whose factors are finite too)
+      const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
+      Metrics m;
+      xf_sigma_metrics(xf_of(ext_from_pair(s1)), xf_of(ext_from_pair(s2)), xf_of(ref.sigma1), xf_of(ref.sigma2), m);
+      a.reS1[i] = m.reS1;
+      a.reS2[i] = m.reS2;
+      a.kh[i] = m.kappa2.hi;
+      a.kl[i] = m.kappa2.lo;
+      a.ke[i] = static_cast<int32_t>(m.kappa2.e);
+      sf |= m.kappa_inf ? 2u : 0u;
+    }
+    a.sflag[i] = sf;
   }
 }
 // reG of the finite lanes, and which lanes those are
@@ -167,29 +177,43 @@ __global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB)
   for (uint64_t i = gtid(); i < n; i += gstride()) {
     if (!fin[i]) continue;
     const uint32_t f = flags[i];
-    out[i] = xf_ortho(factor_of<T>(q11[i], q12[i], f & bit21, f & bit22));
+    const Mat<T> q = factor_of<T>(q11[i], q12[i], f & bit21, f & bit22);
+#ifdef KOG2_ORTHO_GENERAL  // (the reference's full sequence, for A/B)
+    out[i] = xf_ortho(q);
+#else
+    out[i] = xf_ortho_compact(q.g11, q.g12, q.g21, q.g22);
+#endif
   }
 }
-// run_one on the pieces: the singular values' errors and kappa here; lanes off the Xf route (anything not
-// finite) run metrics() whole on the Ext functions, as in run_one_buf
+// metrics() of a lane off the Xf route (something is not finite), whole, on the Ext functions; the reference
+// singular values again from svd2_ext (ref_sigma's values, bit for bit)
+template <class T>
+__device__ __noinline__ void metrics_whole_ext(const Mat<T> g, const Mat<T> u, const Mat<T> v, const EPair<T> s1,
+                                               const EPair<T> s2, Metrics& m) {
+  ExtSvd ref;
+  svd2_ext<T, false>(g, ref);
+  metrics_ext<T>(g, u, v, ext_from_pair(s1), ext_from_pair(s2), ref, m);
+}
+// run_one on the pieces the split kernels left
 template <class T>
 __device__ __forceinline__ uint32_t run_one_split(const InP<T>& gin, const SvdBuf<T>& b, const StudyAux& a, uint64_t i,
                                                   Metrics& m) {
-  ExtSvd ref;
-  ref.sigma1 = Ext{b.re1[i], b.rh1[i], b.rl1[i]};
-  ref.sigma2 = Ext{b.re2[i], b.rh2[i], b.rl2[i]};
   uint32_t flags = b.flags[i];
-  const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
-  if (a.fin[i] != 0 && ref_sigma_finite(ref)) {
+  const uint32_t sf = a.sflag[i];
+  if (a.fin[i] != 0 && (sf & 1u) != 0) {
     m.reG = a.reG[i];
+    m.reS1 = a.reS1[i];
+    m.reS2 = a.reS2[i];
     m.reU = a.reU[i];
     m.reV = a.reV[i];
-    xf_sigma_metrics(xf_of(ext_from_pair(s1)), xf_of(ext_from_pair(s2)), xf_of(ref.sigma1), xf_of(ref.sigma2), m);
+    m.kappa2 = Ext{a.ke[i], a.kh[i], a.kl[i]};
+    m.kappa_inf = (sf & 2u) != 0;
   } else {
+    const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
     const Mat<T> u = factor_of<T>(b.u11[i], b.u12[i], flags & KOG_F_SIGN_U21, flags & KOG_F_SIGN_U22);
     const Mat<T> v = factor_of<T>(b.v11[i], b.v12[i], flags & KOG_F_SIGN_V21, flags & KOG_F_SIGN_V22);
     if (!all_finite(u) || !all_finite(v) || !is_finite(s1.f) || !is_finite(s2.f)) flags |= KOG_M_NONFINITE_FACTOR;
-    metrics_ext<T>(load_mat(gin, i), u, v, ext_from_pair(s1), ext_from_pair(s2), ref, m);
+    metrics_whole_ext<T>(load_mat(gin, i), u, v, s1, s2, m);
   }
   if (isnan(m.reG) || isnan(m.reS1) || isnan(m.reS2) || isnan(m.reU) || isnan(m.reV)) flags |= KOG_M_NAN_METRIC;
   return flags;
@@ -515,8 +539,12 @@ int study_streams_mode() {
 // the metrics as separate kernels (default) or inside k_study (KOG2_STUDY_SPLIT=0, for A/B)
 bool study_split() {
   static const bool v = [] {
+#ifdef KOG2_STUDY_REF_KERNEL
+    return false;
+#else
     const char* e = std::getenv("KOG2_STUDY_SPLIT");
     return !(e && e[0] == '0');
+#endif
   }();
   return v;
 }
@@ -568,9 +596,10 @@ template <class T>
 int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats, int sms, cudaStream_t st) {
   const uint64_t C = n < kStudyChunk ? n : kStudyChunk;
   const int nbuf = n > C ? 2 : 1;  // two chunk buffers when there is more than one chunk
-  // per matrix: the reference singular values (6 x 8 B), reG/reU/reV (3 x 8 B), the input and the compact
-  // decomposition (10 T), exponents and flags (4 x 4 B), the finite-lane marks (4 B)
-  const size_t per = static_cast<size_t>(C) * (9 * 8 + 10 * sizeof(T) + 5 * sizeof(int32_t));
+  // per matrix: nine 8-byte arrays (the split kernels' pieces: five metrics and kappa_2's significand, or the
+  // reference singular values of the A/B route), the input and the compact decomposition (10 T), exponents
+  // and flags (4 x 4 B), kappa_2's exponent and the two lane marks (3 x 4 B)
+  const size_t per = static_cast<size_t>(C) * (9 * 8 + 10 * sizeof(T) + 7 * sizeof(int32_t));
   const int gmax = study_grid(C, sms, study_bps());
   // one set of per-block kappa slots per consumer stream (concurrent k_study
   // launches never share a slot) after the chunk buffers
@@ -616,7 +645,9 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
     long long* rq = reinterpret_cast<long long*>(rd);
     T* t = reinterpret_cast<T*>(rd + 9 * C);
     int32_t* w = reinterpret_cast<int32_t*>(t + 10 * C);
-    bufs[k].aux = StudyAux{rd + 6 * C, rd + 7 * C, rd + 8 * C, reinterpret_cast<uint32_t*>(w + 4 * C)};
+    // (the split kernels' pieces reuse the reference-sigma arrays of the KOG2_STUDY_REF_KERNEL A/B route)
+    bufs[k].aux = StudyAux{rd + 6 * C, rd + 7 * C, rd + 8 * C, rd, rd + C, rd + 2 * C, rd + 3 * C, w + 4 * C,
+                           reinterpret_cast<uint32_t*>(w + 5 * C), reinterpret_cast<uint32_t*>(w + 6 * C)};
     bufs[k].gm = typename Abi<T>::Mat{t, t + C, t + 2 * C, t + 3 * C};
     const typename Abi<T>::Out om{t + 4 * C, t + 5 * C, w,         w + C,     t + 6 * C,
                                   t + 7 * C, t + 8 * C, t + 9 * C, w + 2 * C, reinterpret_cast<uint32_t*>(w + 3 * C)};
@@ -663,7 +694,7 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
     const int grid = study_grid(len, sms, study_bps());
     if (study_split()) {
       const int gs = grid_for(len);
-      k_study_sigma<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.sb, len);
+      k_study_sigma<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.sb, bf.aux, len);
       if ((rc = launched("k_study_sigma")) != KOG_OK) break;
       k_study_recon<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.sb, bf.aux, len);
       if ((rc = launched("k_study_recon")) != KOG_OK) break;
