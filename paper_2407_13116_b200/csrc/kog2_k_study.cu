@@ -120,6 +120,8 @@ __device__ __forceinline__ uint32_t run_one_buf(const Mat<T>& g, const SvdBuf<T>
 struct StudyAux {
   double *reG, *reU, *reV, *reS1, *reS2, *kh, *kl;  // kappa_2 = (ke, kh, kl)
   int32_t* ke;
+  double *xh3, *xl3;   // between k_study_urv and k_study_sigma: the third intermediate (the first two in the
+  int32_t *xe2, *xe3;  // result slots)
   uint32_t* sflag;  // bit 0: the reference singular values are finite; bit 1: kappa_inf
   uint32_t* fin;    // g, u, v and the computed singular values are finite (with bit 0 above: metrics()'s Xf route)
 };
@@ -130,21 +132,59 @@ __device__ __forceinline__ Mat<T> factor_of(T q11, T q12, bool neg21, bool neg22
   return Mat<T>{q11, q12, with_sign(fabs(q12), neg21), with_sign(fabs(q11), neg22)};
 }
 
+// Blocks of 256 threads per SM the split kernels are compiled for.  With their loops in the instruction cache,
+// occupancy pays (launch list r11, us per 2^22 chunk at 2 / 3 / 4 blocks: urv 349 / 326 / 314, sigma 391 / 317 /
+// 287, recon 459 / 437 / 438) — the opposite of the fused kernel, where more warps only fought over the cache.
 #ifndef KOG2_SPLIT_MINB
-#define KOG2_SPLIT_MINB 2
+#define KOG2_SPLIT_MINB 4
 #endif
-// svd2_ext's singular values (ref_sigma: inline Xf where it applies) of a chunk
+#ifndef KOG2_ABSORB_MINB
+#define KOG2_ABSORB_MINB 4
+#endif
+// svd2_ext's singular values in two launches.  First the triangular factor (r11, r12, r22) of the lanes on the
+// Xf route (ref_urv_xf), kept in the slots the second launch overwrites with its results — or, for the other
+// lanes, the singular values themselves from svd2_ext; sflag says which (0 values, 1 factor, 2 factor with
+// r22 = 0).
 template <class T>
-__global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_sigma(InP<T> in, SvdBuf<T> b, StudyAux a, uint64_t n) {
+__global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_urv(InP<T> in, StudyAux a, uint64_t n) {
   for (uint64_t i = gtid(); i < n; i += gstride()) {
-    ExtSvd ref;
-    ref_sigma<T>(load_mat(in, i), ref);
-    const bool rf = ref_sigma_finite(ref);
+    const Mat<T> g = load_mat(in, i);
+    Xf x1, x2, x3 = xf_zero();
+    const int kind = ref_urv_xf(g, x1, x2, x3);
+    if (kind == 0) {
+      ExtSvd ref;
+      svd2_ext<T, false>(g, ref);
+      x1 = xf_of(ref.sigma1);  // (a finite value's exponent fits; the others are not read as numbers)
+      x2 = xf_of(ref.sigma2);
+    }
+    a.reS1[i] = x1.hi;
+    a.reS2[i] = x1.lo;
+    a.ke[i] = x1.e;
+    a.kh[i] = x2.hi;
+    a.kl[i] = x2.lo;
+    a.xe2[i] = x2.e;
+    a.xh3[i] = x3.hi;
+    a.xl3[i] = x3.lo;
+    a.xe3[i] = x3.e;
+    a.sflag[i] = static_cast<uint32_t>(kind);
+  }
+}
+// then the singular values (ref_tri_xf), their errors and kappa_2
+template <class T>
+__global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_sigma(SvdBuf<T> b, StudyAux a, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const int kind = static_cast<int>(a.sflag[i]);
+    Xf ref1{a.ke[i], a.reS1[i], a.reS2[i]}, ref2{a.xe2[i], a.kh[i], a.kl[i]};
+    if (kind != 0) {
+      const Xf r11 = ref1, r12 = ref2, r22{a.xe3[i], a.xh3[i], a.xl3[i]};
+      ref_tri_xf(kind, r11, r12, r22, ref1, ref2);
+    }
+    const bool rf = is_finite(ref1.hi) && is_finite(ref2.hi) && is_finite(ref1.lo) && is_finite(ref2.lo);
     uint32_t sf = rf ? 1u : 0u;
     if (rf) {  // the singular values' errors and kappa_2 (used by the lanes whose factors are finite too)
       const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
       Metrics m;
-      xf_sigma_metrics(xf_of(ext_from_pair(s1)), xf_of(ext_from_pair(s2)), xf_of(ref.sigma1), xf_of(ref.sigma2), m);
+      xf_sigma_metrics(xf_of(ext_from_pair(s1)), xf_of(ext_from_pair(s2)), ref1, ref2, m);
       a.reS1[i] = m.reS1;
       a.reS2[i] = m.reS2;
       a.kh[i] = m.kappa2.hi;
@@ -268,6 +308,39 @@ __device__ __forceinline__ bool kappa_better(const Ext& a, unsigned long long ia
   return c > 0 || (c == 0 && ia < ib);
 }
 
+// the lanes' packed byte counters into the block's 19 shared counts (t2p[7], path[7], then the five flags in
+// BranchCounts' order: tanpsi_inf, diag_swap, compose_minus, sigma_swap, prescale_inexact = bits 10, 11, 13, 12, 14)
+__device__ __forceinline__ void flush_counts(unsigned* cnt, unsigned long long t2p, unsigned long long path,
+                                             unsigned long long fl) {
+  const unsigned active = __activemask();
+  const bool leader = (threadIdx.x & 31u) == static_cast<unsigned>(__ffs(active) - 1);
+#pragma unroll
+  for (unsigned k = 0; k < 7; ++k) {
+    const unsigned a = __reduce_add_sync(active, static_cast<unsigned>(t2p >> (8u * k)) & 255u);
+    const unsigned b = __reduce_add_sync(active, static_cast<unsigned>(path >> (8u * k)) & 255u);
+    if (leader && a) atomicAdd(&cnt[k], a);
+    if (leader && b) atomicAdd(&cnt[7 + k], b);
+  }
+  const int slot[5] = {14, 15, 17, 16, 18};
+#pragma unroll
+  for (unsigned k = 0; k < 5; ++k) {
+    const unsigned a = __reduce_add_sync(active, static_cast<unsigned>(fl >> (8u * k)) & 255u);
+    if (leader && a) atomicAdd(&cnt[slot[k]], a);
+  }
+}
+
+// a > b under ext_cmp for the absorb's running maximum.  Positive canonical values (significands in
+// [1 - 2^-54, 2)) whose exponents lie two or more apart are ordered by the exponents; the others take the
+// subtraction as the reference does.
+__device__ __forceinline__ bool kappa_gt(const Ext& a, const Ext& b) {
+  if (a.hi > 0.0 && b.hi > 0.0) {
+    const long long d = a.e - b.e;
+    if (d >= 2) return true;
+    if (d <= -2) return false;
+  }
+  return xf_cmp(xf_of(a), xf_of(b)) > 0;
+}
+
 struct BlockPartial {
   kog_extfloat k;
   unsigned long long idx;
@@ -290,7 +363,7 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 #endif
 constexpr int kStudyThreads = KOG2_STUDY_THREADS;
 template <class T, int ROUTINE, int PHASED>  // PHASED: 0 fused, 1 from the chunk's svd2 buffers, 2 from the split kernels' pieces too
-__global__ void __launch_bounds__(kStudyThreads, KOG2_STUDY_MINB)
+__global__ void __launch_bounds__(kStudyThreads, PHASED == 2 ? KOG2_ABSORB_MINB : KOG2_STUDY_MINB)
     k_study(GenCfg c, uint64_t index0, uint64_t n, Opt opt, kog_stats* stats, BlockPartial* partial, InP<T> gin,
             SvdBuf<T> sb, bool accumulate, StudyAux aux) {
   __shared__ unsigned cnt[19];
@@ -306,6 +379,8 @@ __global__ void __launch_bounds__(kStudyThreads, KOG2_STUDY_MINB)
   bool kinf = false;
   unsigned long long fail = ~0ull;
   const unsigned lane = threadIdx.x & 31u;
+  unsigned long long c_t2p = 0ull, c_path = 0ull, c_fl = 0ull;  // 7 + 7 + 5 counts, one byte each
+  unsigned absorbed = 0u;
 
   for (uint64_t i = gtid(); i < n; i += gstride()) {
     const unsigned long long index = index0 + i;
@@ -340,40 +415,27 @@ __global__ void __launch_bounds__(kStudyThreads, KOG2_STUDY_MINB)
       mV = fmax(mV, m.reV);
       if (m.kappa_inf) {
         kinf = true;
-      } else if (xf_cmp(xf_of(m.kappa2), xf_of(kb.k)) > 0) {  // kb.k starts at zero like maxKappa2
+      } else if (kappa_gt(m.kappa2, kb.k)) {  // kb.k starts at zero like maxKappa2
         kb.k = m.kappa2;  // a lane's indices increase: first occurrence kept
         kb.idx = index;
         kb.valid = true;
       }
     }
-    if (ROUTINE == KOG_ROUTINE_KOG) {  // BranchCounts::add (harness.hpp:56-64)
-      const unsigned active = __activemask();
-      const unsigned path = (flags >> KOG_F_PATH_SHIFT) & 7u;
-      const unsigned t2p = (flags >> KOG_F_T2P_SHIFT) & 7u;
-      const int leader = __ffs(active) - 1;
-#pragma unroll
-      for (unsigned k = 0; k < 7; ++k) {
-        const unsigned bt = __ballot_sync(active, ok && t2p == k);
-        const unsigned bp = __ballot_sync(active, ok && path == k);
-        if (static_cast<int>(lane) == leader) {
-          if (bt) atomicAdd(&cnt[k], __popc(bt));
-          if (bp) atomicAdd(&cnt[7 + k], __popc(bp));
-        }
+    if (ROUTINE == KOG_ROUTINE_KOG) {  // BranchCounts::add (harness.hpp:56-64), into this thread's packed counters
+      if (ok) {
+        c_t2p += 1ull << (8u * ((flags >> KOG_F_T2P_SHIFT) & 7u));
+        c_path += 1ull << (8u * ((flags >> KOG_F_PATH_SHIFT) & 7u));
+        // flag bits 10..14, bit j to byte j (the multiplier's five copies put bit j at 8j; no two terms meet)
+        c_fl += (static_cast<unsigned long long>((flags >> 10) & 31u) * 0x10204081ull) & 0x0101010101ull;
       }
-      const unsigned b0 = __ballot_sync(active, ok && (flags & KOG_F_TANPSI_INF));
-      const unsigned b1 = __ballot_sync(active, ok && (flags & KOG_F_DIAG_SWAP));
-      const unsigned b2 = __ballot_sync(active, ok && (flags & KOG_F_COMPOSE_MINUS));
-      const unsigned b3 = __ballot_sync(active, ok && (flags & KOG_F_SIGMA_SWAP));
-      const unsigned b4 = __ballot_sync(active, ok && (flags & KOG_F_PRESCALE_INEXACT));
-      if (static_cast<int>(lane) == leader) {
-        if (b0) atomicAdd(&cnt[14], __popc(b0));
-        if (b1) atomicAdd(&cnt[15], __popc(b1));
-        if (b2) atomicAdd(&cnt[16], __popc(b2));
-        if (b3) atomicAdd(&cnt[17], __popc(b3));
-        if (b4) atomicAdd(&cnt[18], __popc(b4));
+      if (++absorbed == 255u) {  // (one byte per count; the lanes of a warp get here together)
+        flush_counts(cnt, c_t2p, c_path, c_fl);
+        c_t2p = c_path = c_fl = 0ull;
+        absorbed = 0u;
       }
     }
   }
+  if (ROUTINE == KOG_ROUTINE_KOG) flush_counts(cnt, c_t2p, c_path, c_fl);
 
   // ---- warp reduction (every lane participates)
   for (int off = 16; off > 0; off >>= 1) {
@@ -517,7 +579,7 @@ int launch_ext(const MatC* g, kog_extsvd* o, uint64_t n, cudaStream_t st) {
 #define KOG2_STUDY_STREAMS_DEFAULT 1  // two consumer streams ran two k_study at once: erratic 500-1500 M/s at 2^31
 #endif
 #ifndef KOG2_STUDY_BPS_DEFAULT
-#define KOG2_STUDY_BPS_DEFAULT 8
+#define KOG2_STUDY_BPS_DEFAULT 4  // the absorb kernel's resident blocks: one wave, one epilogue per block (r11: 8 -> 168 us, 4 -> 154 us, 16 -> 197 us)
 #endif
 // grid of the study kernels: at most `per_sm` blocks per SM (grid-stride loops)
 int study_grid(uint64_t n, int sms, int per_sm = 8) {
@@ -598,8 +660,8 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
   const int nbuf = n > C ? 2 : 1;  // two chunk buffers when there is more than one chunk
   // per matrix: nine 8-byte arrays (the split kernels' pieces: five metrics and kappa_2's significand, or the
   // reference singular values of the A/B route), the input and the compact decomposition (10 T), exponents
-  // and flags (4 x 4 B), kappa_2's exponent and the two lane marks (3 x 4 B)
-  const size_t per = static_cast<size_t>(C) * (9 * 8 + 10 * sizeof(T) + 7 * sizeof(int32_t));
+  // and flags (4 x 4 B), kappa_2's exponent, the two lane marks and two intermediate exponents (5 x 4 B)
+  const size_t per = static_cast<size_t>(C) * (9 * 8 + 10 * sizeof(T) + 9 * sizeof(int32_t));
   const int gmax = study_grid(C, sms, study_bps());
   // one set of per-block kappa slots per consumer stream (concurrent k_study
   // launches never share a slot) after the chunk buffers
@@ -646,8 +708,9 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
     T* t = reinterpret_cast<T*>(rd + 9 * C);
     int32_t* w = reinterpret_cast<int32_t*>(t + 10 * C);
     // (the split kernels' pieces reuse the reference-sigma arrays of the KOG2_STUDY_REF_KERNEL A/B route)
-    bufs[k].aux = StudyAux{rd + 6 * C, rd + 7 * C, rd + 8 * C, rd, rd + C, rd + 2 * C, rd + 3 * C, w + 4 * C,
-                           reinterpret_cast<uint32_t*>(w + 5 * C), reinterpret_cast<uint32_t*>(w + 6 * C)};
+    bufs[k].aux = StudyAux{rd + 6 * C, rd + 7 * C, rd + 8 * C, rd,        rd + C,    rd + 2 * C, rd + 3 * C,
+                           w + 4 * C,  rd + 4 * C, rd + 5 * C, w + 7 * C, w + 8 * C, reinterpret_cast<uint32_t*>(w + 5 * C),
+                           reinterpret_cast<uint32_t*>(w + 6 * C)};
     bufs[k].gm = typename Abi<T>::Mat{t, t + C, t + 2 * C, t + 3 * C};
     const typename Abi<T>::Out om{t + 4 * C, t + 5 * C, w,         w + C,     t + 6 * C,
                                   t + 7 * C, t + 8 * C, t + 9 * C, w + 2 * C, reinterpret_cast<uint32_t*>(w + 3 * C)};
@@ -694,7 +757,9 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
     const int grid = study_grid(len, sms, study_bps());
     if (study_split()) {
       const int gs = grid_for(len);
-      k_study_sigma<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.sb, bf.aux, len);
+      k_study_urv<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.aux, len);
+      if ((rc = launched("k_study_urv")) != KOG_OK) break;
+      k_study_sigma<T><<<gs, kThreads, 0, q>>>(bf.sb, bf.aux, len);
       if ((rc = launched("k_study_sigma")) != KOG_OK) break;
       k_study_recon<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.sb, bf.aux, len);
       if ((rc = launched("k_study_recon")) != KOG_OK) break;
