@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_sigma(SvdBu
     a.sflag[i] = sf;
   }
 }
-// reG of the finite lanes, and which lanes those are
+// reG of the finite lanes in two launches: which lanes those are and the squared norm of the residual ...
 template <class T>
 __global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_recon(InP<T> in, SvdBuf<T> b, StudyAux a, uint64_t n) {
   for (uint64_t i = gtid(); i < n; i += gstride()) {
@@ -206,7 +206,22 @@ __global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_recon(InP<T
     const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
     const bool fin = mat_finite(g) && mat_finite(u) && mat_finite(v) && is_finite(s1.f) && is_finite(s2.f);
     a.fin[i] = fin ? 1u : 0u;
-    if (fin) a.reG[i] = xf_recon(g, u, v, xf_of(ext_from_pair(s1)), xf_of(ext_from_pair(s2)));
+    Xf sq = xf_zero();
+    if (fin) sq = xf_recon_sq(g, u, v, xf_of(ext_from_pair(s1)), xf_of(ext_from_pair(s2)));
+    a.xh3[i] = sq.hi;
+    a.xl3[i] = sq.lo;
+    a.xe3[i] = sq.e;
+  }
+}
+// ... then its root over ||G||_F
+template <class T>
+__global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_ratio(InP<T> in, StudyAux a, uint64_t n) {
+  for (uint64_t i = gtid(); i < n; i += gstride()) {
+    const Mat<T> g = load_mat(in, i);
+    const Xf sq{a.xe3[i], a.xh3[i], a.xl3[i]};
+    double r = 0.0;
+    if (a.fin[i] != 0) r = xf_recon_ratio(g, sq);
+    a.reG[i] = r;
   }
 }
 // the orthogonality defect of one factor (launched for U and for V) of the finite lanes
@@ -215,7 +230,10 @@ __global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB)
     k_study_ortho(const T* q11, const T* q12, const uint32_t* flags, uint32_t bit21, uint32_t bit22,
                   const uint32_t* fin, double* out, uint64_t n) {
   for (uint64_t i = gtid(); i < n; i += gstride()) {
-    if (!fin[i]) continue;
+    if (!fin[i]) {
+      out[i] = 0.0;  // (not used: the lane runs metrics() whole in the absorb kernel)
+      continue;
+    }
     const uint32_t f = flags[i];
     const Mat<T> q = factor_of<T>(q11[i], q12[i], f & bit21, f & bit22);
 #ifdef KOG2_ORTHO_GENERAL  // (the reference's full sequence, for A/B)
@@ -238,17 +256,18 @@ __device__ __noinline__ void metrics_whole_ext(const Mat<T> g, const Mat<T> u, c
 template <class T>
 __device__ __forceinline__ uint32_t run_one_split(const InP<T>& gin, const SvdBuf<T>& b, const StudyAux& a, uint64_t i,
                                                   Metrics& m) {
+  // every piece is loaded before the lane marks are looked at (one memory round trip per matrix, not two; the
+  // slots of a lane off the Xf route hold zeros or intermediates that are not used)
   uint32_t flags = b.flags[i];
-  const uint32_t sf = a.sflag[i];
-  if (a.fin[i] != 0 && (sf & 1u) != 0) {
-    m.reG = a.reG[i];
-    m.reS1 = a.reS1[i];
-    m.reS2 = a.reS2[i];
-    m.reU = a.reU[i];
-    m.reV = a.reV[i];
-    m.kappa2 = Ext{a.ke[i], a.kh[i], a.kl[i]};
-    m.kappa_inf = (sf & 2u) != 0;
-  } else {
+  const uint32_t sf = a.sflag[i], fin = a.fin[i];
+  m.reG = a.reG[i];
+  m.reS1 = a.reS1[i];
+  m.reS2 = a.reS2[i];
+  m.reU = a.reU[i];
+  m.reV = a.reV[i];
+  m.kappa2 = Ext{a.ke[i], a.kh[i], a.kl[i]};
+  m.kappa_inf = (sf & 2u) != 0;
+  if (fin == 0 || (sf & 1u) == 0) {
     const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
     const Mat<T> u = factor_of<T>(b.u11[i], b.u12[i], flags & KOG_F_SIGN_U21, flags & KOG_F_SIGN_U22);
     const Mat<T> v = factor_of<T>(b.v11[i], b.v12[i], flags & KOG_F_SIGN_V21, flags & KOG_F_SIGN_V22);
@@ -763,6 +782,8 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
       if ((rc = launched("k_study_sigma")) != KOG_OK) break;
       k_study_recon<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.sb, bf.aux, len);
       if ((rc = launched("k_study_recon")) != KOG_OK) break;
+      k_study_ratio<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.aux, len);
+      if ((rc = launched("k_study_ratio")) != KOG_OK) break;
       k_study_ortho<T><<<gs, kThreads, 0, q>>>(bf.sb.u11, bf.sb.u12, bf.sb.flags, KOG_F_SIGN_U21, KOG_F_SIGN_U22,
                                                bf.aux.fin, bf.aux.reU, len);
       if ((rc = launched("k_study_ortho")) != KOG_OK) break;
