@@ -124,6 +124,7 @@ struct StudyAux {
   int32_t *xe2, *xe3;  // result slots)
   uint32_t* sflag;  // bit 0: the reference singular values are finite; bit 1: kappa_inf
   uint32_t* fin;    // g, u, v and the computed singular values are finite (with bit 0 above: metrics()'s Xf route)
+  uint32_t *list, *count;  // the chunk's lanes off that route (k_study_whole's work list)
 };
 
 // the factors as run_one_buf expands them
@@ -225,13 +226,18 @@ __global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_ratio(InP<T
   }
 }
 // the orthogonality defect of one factor (launched for U and for V) of the finite lanes
-template <class T>
+// (LIST: this launch — the last one, fin and sflag are final — also collects the lanes off the Xf route)
+template <class T, bool LIST>
 __global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB)
     k_study_ortho(const T* q11, const T* q12, const uint32_t* flags, uint32_t bit21, uint32_t bit22,
-                  const uint32_t* fin, double* out, uint64_t n) {
+                  const uint32_t* fin, double* out, uint64_t n, StudyAux a) {
   for (uint64_t i = gtid(); i < n; i += gstride()) {
-    if (!fin[i]) {
-      out[i] = 0.0;  // (not used: the lane runs metrics() whole in the absorb kernel)
+    const bool xf_lane = fin[i] != 0;
+    if constexpr (LIST) {
+      if (!xf_lane || (a.sflag[i] & 1u) == 0) a.list[atomicAdd(a.count, 1u)] = static_cast<uint32_t>(i);
+    }
+    if (!xf_lane) {
+      out[i] = 0.0;  // (not used: k_study_whole writes the lane's metrics)
       continue;
     }
     const uint32_t f = flags[i];
@@ -252,28 +258,52 @@ __device__ __noinline__ void metrics_whole_ext(const Mat<T> g, const Mat<T> u, c
   svd2_ext<T, false>(g, ref);
   metrics_ext<T>(g, u, v, ext_from_pair(s1), ext_from_pair(s2), ref, m);
 }
+// The lanes off the Xf route (something is not finite; rare): metrics() whole, written into the same slots, so
+// that the absorb kernel below only reads (a scan for these lanes inside a kernel holding this code ran at its 152
+// registers: 126 us per chunk; the list costs nothing).  sflag afterwards: bit 1 kappa_inf, bit 2 KOG_M_NONFINITE_FACTOR, bit 3
+// kappa_2's exponent does not fit 32 bits (its high word is in xe2).
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_study_whole(InP<T> gin, SvdBuf<T> b, StudyAux a) {
+  const uint64_t m_count = *a.count;
+  for (uint64_t k = gtid(); k < m_count; k += gstride()) {
+    const uint64_t i = a.list[k];
+    const uint32_t flags = b.flags[i];
+    const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
+    const Mat<T> u = factor_of<T>(b.u11[i], b.u12[i], flags & KOG_F_SIGN_U21, flags & KOG_F_SIGN_U22);
+    const Mat<T> v = factor_of<T>(b.v11[i], b.v12[i], flags & KOG_F_SIGN_V21, flags & KOG_F_SIGN_V22);
+    const bool nonfinite = !all_finite(u) || !all_finite(v) || !is_finite(s1.f) || !is_finite(s2.f);
+    Metrics m;
+    metrics_whole_ext<T>(load_mat(gin, i), u, v, s1, s2, m);
+    a.reG[i] = m.reG;
+    a.reS1[i] = m.reS1;
+    a.reS2[i] = m.reS2;
+    a.reU[i] = m.reU;
+    a.reV[i] = m.reV;
+    a.kh[i] = m.kappa2.hi;
+    a.kl[i] = m.kappa2.lo;
+    const int32_t lo = static_cast<int32_t>(m.kappa2.e);
+    const bool wide = static_cast<long long>(lo) != m.kappa2.e;
+    a.ke[i] = lo;
+    if (wide) a.xe2[i] = static_cast<int32_t>(m.kappa2.e >> 32);
+    a.sflag[i] = 1u | (m.kappa_inf ? 2u : 0u) | (nonfinite ? 4u : 0u) | (wide ? 8u : 0u);
+  }
+}
 // run_one on the pieces the split kernels left
 template <class T>
-__device__ __forceinline__ uint32_t run_one_split(const InP<T>& gin, const SvdBuf<T>& b, const StudyAux& a, uint64_t i,
-                                                  Metrics& m) {
-  // every piece is loaded before the lane marks are looked at (one memory round trip per matrix, not two; the
-  // slots of a lane off the Xf route hold zeros or intermediates that are not used)
+__device__ __forceinline__ uint32_t run_one_split(const SvdBuf<T>& b, const StudyAux& a, uint64_t i, Metrics& m) {
   uint32_t flags = b.flags[i];
-  const uint32_t sf = a.sflag[i], fin = a.fin[i];
+  const uint32_t sf = a.sflag[i];
   m.reG = a.reG[i];
   m.reS1 = a.reS1[i];
   m.reS2 = a.reS2[i];
   m.reU = a.reU[i];
   m.reV = a.reV[i];
-  m.kappa2 = Ext{a.ke[i], a.kh[i], a.kl[i]};
+  const int32_t ke = a.ke[i];
+  long long e = ke;
+  if (sf & 8u) e = (static_cast<long long>(a.xe2[i]) << 32) | static_cast<uint32_t>(ke);
+  m.kappa2 = Ext{e, a.kh[i], a.kl[i]};
   m.kappa_inf = (sf & 2u) != 0;
-  if (fin == 0 || (sf & 1u) == 0) {
-    const EPair<T> s1{b.sig1_e[i], b.sig1_f[i]}, s2{b.sig2_e[i], b.sig2_f[i]};
-    const Mat<T> u = factor_of<T>(b.u11[i], b.u12[i], flags & KOG_F_SIGN_U21, flags & KOG_F_SIGN_U22);
-    const Mat<T> v = factor_of<T>(b.v11[i], b.v12[i], flags & KOG_F_SIGN_V21, flags & KOG_F_SIGN_V22);
-    if (!all_finite(u) || !all_finite(v) || !is_finite(s1.f) || !is_finite(s2.f)) flags |= KOG_M_NONFINITE_FACTOR;
-    metrics_whole_ext<T>(load_mat(gin, i), u, v, s1, s2, m);
-  }
+  if (sf & 4u) flags |= KOG_M_NONFINITE_FACTOR;
   if (isnan(m.reG) || isnan(m.reS1) || isnan(m.reS2) || isnan(m.reU) || isnan(m.reV)) flags |= KOG_M_NAN_METRIC;
   return flags;
 }
@@ -406,7 +436,7 @@ __global__ void __launch_bounds__(kStudyThreads, PHASED == 2 ? KOG2_ABSORB_MINB 
     Metrics m;
     uint32_t flags;
     if constexpr (PHASED == 2) {
-      flags = run_one_split<T>(gin, sb, aux, i, m);
+      flags = run_one_split<T>(sb, aux, i, m);
     } else if constexpr (PHASED == 1) {  // generated and decomposed by the earlier launches of this chunk
       flags = run_one_buf<T>(load_mat(gin, i), sb, i, m);
     } else {
@@ -679,13 +709,13 @@ int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_sta
   const int nbuf = n > C ? 2 : 1;  // two chunk buffers when there is more than one chunk
   // per matrix: nine 8-byte arrays (the split kernels' pieces: five metrics and kappa_2's significand, or the
   // reference singular values of the A/B route), the input and the compact decomposition (10 T), exponents
-  // and flags (4 x 4 B), kappa_2's exponent, the two lane marks and two intermediate exponents (5 x 4 B)
-  const size_t per = static_cast<size_t>(C) * (9 * 8 + 10 * sizeof(T) + 9 * sizeof(int32_t));
+  // and flags (4 x 4 B), kappa_2's exponent, the two lane marks, two intermediate exponents and the work list (6 x 4 B)
+  const size_t per = static_cast<size_t>(C) * (9 * 8 + 10 * sizeof(T) + 10 * sizeof(int32_t));
   const int gmax = study_grid(C, sms, study_bps());
   // one set of per-block kappa slots per consumer stream (concurrent k_study
   // launches never share a slot) after the chunk buffers
   const size_t part_off = (per * nbuf + 255) / 256 * 256;
-  const size_t need = part_off + sizeof(BlockPartial) * 2 * gmax;
+  const size_t need = part_off + sizeof(BlockPartial) * 2 * gmax + 2 * sizeof(uint32_t);  // + the lists' counters
   char* ws = static_cast<char*>(kog2_ws_alloc(need, st));
   if (!ws) return KOG_ERR_CUDA;
   BlockPartial* part = reinterpret_cast<BlockPartial*>(ws + part_off);
@@ -729,7 +759,8 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
     // (the split kernels' pieces reuse the reference-sigma arrays of the KOG2_STUDY_REF_KERNEL A/B route)
     bufs[k].aux = StudyAux{rd + 6 * C, rd + 7 * C, rd + 8 * C, rd,        rd + C,    rd + 2 * C, rd + 3 * C,
                            w + 4 * C,  rd + 4 * C, rd + 5 * C, w + 7 * C, w + 8 * C, reinterpret_cast<uint32_t*>(w + 5 * C),
-                           reinterpret_cast<uint32_t*>(w + 6 * C)};
+                           reinterpret_cast<uint32_t*>(w + 6 * C), reinterpret_cast<uint32_t*>(w + 9 * C),
+                           reinterpret_cast<uint32_t*>(part + 2 * gmax) + k};
     bufs[k].gm = typename Abi<T>::Mat{t, t + C, t + 2 * C, t + 3 * C};
     const typename Abi<T>::Out om{t + 4 * C, t + 5 * C, w,         w + C,     t + 6 * C,
                                   t + 7 * C, t + 8 * C, t + 9 * C, w + 2 * C, reinterpret_cast<uint32_t*>(w + 3 * C)};
@@ -784,12 +815,18 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
       if ((rc = launched("k_study_recon")) != KOG_OK) break;
       k_study_ratio<T><<<gs, kThreads, 0, q>>>(bf.gin, bf.aux, len);
       if ((rc = launched("k_study_ratio")) != KOG_OK) break;
-      k_study_ortho<T><<<gs, kThreads, 0, q>>>(bf.sb.u11, bf.sb.u12, bf.sb.flags, KOG_F_SIGN_U21, KOG_F_SIGN_U22,
-                                               bf.aux.fin, bf.aux.reU, len);
+      if (cudaMemsetAsync(bf.aux.count, 0, sizeof(uint32_t), q) != cudaSuccess) {
+        rc = kog2_cuda_error("cudaMemsetAsync(study list)");
+        break;
+      }
+      k_study_ortho<T, false><<<gs, kThreads, 0, q>>>(bf.sb.u11, bf.sb.u12, bf.sb.flags, KOG_F_SIGN_U21,
+                                                      KOG_F_SIGN_U22, bf.aux.fin, bf.aux.reU, len, bf.aux);
       if ((rc = launched("k_study_ortho")) != KOG_OK) break;
-      k_study_ortho<T><<<gs, kThreads, 0, q>>>(bf.sb.v11, bf.sb.v12, bf.sb.flags, KOG_F_SIGN_V21, KOG_F_SIGN_V22,
-                                               bf.aux.fin, bf.aux.reV, len);
+      k_study_ortho<T, true><<<gs, kThreads, 0, q>>>(bf.sb.v11, bf.sb.v12, bf.sb.flags, KOG_F_SIGN_V21,
+                                                     KOG_F_SIGN_V22, bf.aux.fin, bf.aux.reV, len, bf.aux);
       if ((rc = launched("k_study_ortho")) != KOG_OK) break;
+      k_study_whole<T><<<sms, kThreads, 0, q>>>(bf.gin, bf.sb, bf.aux);
+      if ((rc = launched("k_study_whole")) != KOG_OK) break;
       k_study<T, KOG_ROUTINE_KOG, 2><<<grid, kStudyThreads, 0, q>>>(GenCfg{}, index0 + lo, len, Opt{}, stats,
                                                                     part + k * gmax, bf.gin, bf.sb, true, bf.aux);
     } else {
