@@ -181,6 +181,7 @@ PROTOTYPES: dict[str, tuple] = {
     "kog_svd2_deferred_count": (C.c_int64, []),
     "kog_svd2_lean_count": (C.c_int64, []),
     "kog_svd2_set_lean_min": (C.c_uint64, [C.c_uint64]),
+    "kog_study_set_chunk_log2": (C.c_int, [C.c_int]),
     "kog_div_batch_f64": (i32, [P, P, P, u64, P]),
     "kog_div_batch_f32": (i32, [P, P, P, u64, P]),
     "kog_launch_count": (C.c_uint64, []),
@@ -233,6 +234,8 @@ def load(path: str | None = None) -> C.CDLL:
         fn.argtypes = args
     if os.environ.get("KOG2_LEAN_MIN_LOG2"):  # tuning runs (tools/lean_sizes.sh): the two-speed kernel's threshold
         lib.kog_svd2_set_lean_min(1 << int(os.environ["KOG2_LEAN_MIN_LOG2"]))
+    if os.environ.get("KOG2_STUDY_CHUNK_LOG2"):  # tuning runs: the phased study's chunk
+        lib.kog_study_set_chunk_log2(int(os.environ["KOG2_STUDY_CHUNK_LOG2"]))
     if path is None:
         _lib = lib
     return lib

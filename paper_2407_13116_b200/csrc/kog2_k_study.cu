@@ -3,6 +3,7 @@
 // and the fused study kernel generate -> svd2_ext -> svd2 | lasv2 ->
 // finiteness -> metrics -> ErrorStats absorb (harness.hpp:190-222), reduced
 // with warp shuffles, shared memory and order-independent global atomics.
+#include <atomic>
 #include <cstdlib>
 
 #include "kog2_common.cuh"
@@ -669,7 +670,13 @@ int study_bps() {
   return v;
 }
 
-constexpr uint64_t kStudyChunk = 1ull << 22;
+// Matrices per chunk of the phased study (kog_study_set_chunk_log2).  2^23 by default: the chunk's svd2 call then
+// takes the two-speed kernel, and the per-chunk launches and tails halve (study over 2^28 config-5 matrices,
+// 10^6/s: 2^21 2,580, 2^22 2,676, 2^23 2,821, 2^24 2,887 at twice the 3.2 GB of chunk buffers).
+#ifndef KOG2_STUDY_CHUNK_LOG2
+#define KOG2_STUDY_CHUNK_LOG2 23
+#endif
+std::atomic<int> g_study_chunk_log2{KOG2_STUDY_CHUNK_LOG2};
 
 template <class T> struct Abi;
 template <> struct Abi<double> {
@@ -705,7 +712,8 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
                      Kog2SideStreams* side);
 template <class T>
 int study_phased(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog_stats* stats, int sms, cudaStream_t st) {
-  const uint64_t C = n < kStudyChunk ? n : kStudyChunk;
+  const uint64_t chunk = 1ull << g_study_chunk_log2.load(std::memory_order_relaxed);
+  const uint64_t C = n < chunk ? n : chunk;
   const int nbuf = n > C ? 2 : 1;  // two chunk buffers when there is more than one chunk
   // per matrix: nine 8-byte arrays (the split kernels' pieces: five metrics and kappa_2's significand, or the
   // reference singular values of the A/B route), the input and the compact decomposition (10 T), exponents
@@ -855,6 +863,11 @@ int study_phased_run(const kog_run_config* cfg, uint64_t index0, uint64_t n, kog
 }  // namespace
 
 extern "C" {
+
+int kog_study_set_chunk_log2(int log2_matrices) {
+  const int v = log2_matrices < 16 ? 16 : (log2_matrices > 26 ? 26 : log2_matrices);
+  return g_study_chunk_log2.exchange(v);
+}
 
 int kog_svd2_ext_batch_f64(const kog_mat_f64* g, kog_extsvd* out, uint64_t n, void* stream) {
   return launch_ext<double>(g, out, n, KOG2_ST(stream));

@@ -146,3 +146,19 @@ def hypot_exact(a: float, b: float, dt) -> float:
 
 def exact_fraction(x: float) -> Fraction:
     return Fraction(x)
+
+
+import contextlib
+
+
+@contextlib.contextmanager
+def study_chunk(log2: int):
+    """The phased study's chunk at 2^log2 matrices for the enclosed calls (kog_study_set_chunk_log2): the
+    multi-chunk pipeline is exercised at counts the CPU reference finishes in seconds."""
+    from paper_2407_13116_b200 import capi
+    lib = capi.load()
+    before = lib.kog_study_set_chunk_log2(log2)
+    try:
+        yield
+    finally:
+        lib.kog_study_set_chunk_log2(before)

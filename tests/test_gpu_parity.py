@@ -703,23 +703,35 @@ def test_run_batch_csv_matches_reference_rows(cuda, row):
 def test_run_batch_vs_reference_counts(cuda, ref):
     """ErrorStats incl. all 19 BranchCounts equal the reference's run_batch
     (harness.hpp:226-271) on the branch-coverage batch of harness_test.cpp:164-217."""
+    wants = {}
     for cfg in (K.RunConfig(shape=capi.SHAPE_GEN, regime=capi.REGIME_BULLET, count=1 << 18, seed=77),
                 K.RunConfig(shape=capi.SHAPE_TRI, regime=capi.REGIME_CIRC, count=1 << 18, seed=78),
                 K.RunConfig(shape=capi.SHAPE_TRI, regime=capi.REGIME_BULLET, count=50000, seed=0x1234ABCD,
                             routine=capi.ROUTINE_LASV2),
                 configs.cfg(3, count=1 << 18), configs.cfg(4, count=1 << 18), configs.cfg(2, count=1 << 18),
-                # more than one 2^22-matrix chunk of the phased study
-                configs.cfg(5, count=(1 << 22) + 4099),
+                # more than one chunk of the phased study (chunks of 2^20 here)
+                (configs.cfg(5, count=(1 << 20) + 4099), 20),
                 # four chunks: both chunk buffers reused by the producer/consumer pipeline, a 5-matrix tail
-                configs.cfg(5, count=3 * (1 << 22) + 5),
+                (configs.cfg(5, count=3 * (1 << 22) + 5), 22),
+                # the same at the default chunk (2^23: the two-speed svd2 kernel inside the study, then a tail chunk)
+                (configs.cfg(5, count=3 * (1 << 22) + 5), None),
                 # non-default Options: the general svd2 kernel inside the study
                 K.RunConfig(shape=capi.SHAPE_GEN, regime=capi.REGIME_BULLET, count=1 << 17, seed=79,
                             options=K.Options(hypot_is_cr=False, ominus_for_d=True)),
                 K.RunConfig(single_precision=True, shape=capi.SHAPE_GEN, regime=capi.REGIME_BULLET, count=1 << 17,
                             seed=80, options=K.Options(hypot_is_cr=False))):
-        st = K.run_batch(cfg)
-        rc, want, msg = refbind.run_batch(ref, cfg.c())
-        assert rc == 0, msg
+        cfg, chunk = cfg if isinstance(cfg, tuple) else (cfg, None)
+        if chunk is None:
+            st = K.run_batch(cfg)
+        else:
+            with _gen.study_chunk(chunk):
+                st = K.run_batch(cfg)
+        key = bytes(cfg.c())
+        if key not in wants:  # (the reference's run_batch over 12.6 million matrices once)
+            rc, want, msg = refbind.run_batch(ref, cfg.c())
+            assert rc == 0, msg
+            wants[key] = want
+        want = wants[key]
         got_row, want_row = K.csv_row(cfg, st).split(","), refbind.csv_row(ref, cfg.c(), want).split(",")
         if cfg.regime == capi.REGIME_RANGED:  # the reference's csv_row has no name for the extension
             got_row[2] = want_row[2]
