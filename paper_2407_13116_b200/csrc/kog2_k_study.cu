@@ -152,8 +152,9 @@ __global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_urv(InP<T> 
   for (uint64_t i = gtid(); i < n; i += gstride()) {
     const Mat<T> g = load_mat(in, i);
     Xf x1, x2, x3 = xf_zero();
-    const int kind = ref_urv_xf(g, x1, x2, x3);
-    if (kind == 0) {
+    int kind = ref_urv_xf(g, x1, x2, x3);
+    if (kind == 3) kind = 0;  // the singular values themselves
+    else if (kind == 0) {
       ExtSvd ref;
       svd2_ext<T, false>(g, ref);
       x1 = xf_of(ref.sigma1);  // (a finite value's exponent fits; the others are not read as numbers)
