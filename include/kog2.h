@@ -438,7 +438,7 @@ int64_t kog_svd2_lean_count(void);
  * previous value.  Results do not depend on it. */
 uint64_t kog_svd2_set_lean_min(uint64_t n);
 /* Tuning knob: log2 of the matrices per chunk of kog_study_batch's pipeline
- * (default 23; clamped to [16, 26]; the chunk buffers take 192 B per matrix,
+ * (default 24; clamped to [16, 26]; the chunk buffers take 192 B per matrix,
  * twice).  Returns the previous value.  Results do not depend on it. */
 int kog_study_set_chunk_log2(int log2_matrices);
 /* number of kernel launches issued by this library since load */

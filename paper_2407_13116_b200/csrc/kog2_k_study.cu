@@ -671,11 +671,12 @@ int study_bps() {
   return v;
 }
 
-// Matrices per chunk of the phased study (kog_study_set_chunk_log2).  2^23 by default: the chunk's svd2 call then
-// takes the two-speed kernel, and the per-chunk launches and tails halve (study over 2^28 config-5 matrices,
-// 10^6/s: 2^21 2,580, 2^22 2,676, 2^23 2,821, 2^24 2,887 at twice the 3.2 GB of chunk buffers).
+// Matrices per chunk of the phased study (kog_study_set_chunk_log2).  2^24 by default: from 2^23 the chunk's svd2
+// call takes the two-speed kernel, and the per-chunk launches and tails shrink with the count (study over 2^28
+// config-5 matrices, 10^6/s: 2^21 2,580, 2^22 2,676, 2^23 2,821, 2^24 2,887; two chunk buffers of 192 B per
+// matrix: 6.4 GB of the 180).
 #ifndef KOG2_STUDY_CHUNK_LOG2
-#define KOG2_STUDY_CHUNK_LOG2 23
+#define KOG2_STUDY_CHUNK_LOG2 24
 #endif
 std::atomic<int> g_study_chunk_log2{KOG2_STUDY_CHUNK_LOG2};
 

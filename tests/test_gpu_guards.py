@@ -177,6 +177,7 @@ def test_study_stats_guard(cuda):
     lib.kog_stats_init(C.byref(init))
     st = A.array(C.sizeof(capi.kog_stats), torch.uint8, np.frombuffer(bytes(init), np.uint8))
     A.inputs.clear()  # it is an in/out argument
-    for cfg in (configs.cfg(5, count=(1 << 23) + 5), configs.cfg(4, count=4097)):
-        capi.check(lib.kog_study_batch(C.byref(cfg.c()), 7, cfg.count, st.data_ptr(), _st()))
+    for cfg in (configs.cfg(5, count=(1 << 22) + 5), configs.cfg(4, count=4097)):
+        with _gen.study_chunk(22):  # (two chunks)
+            capi.check(lib.kog_study_batch(C.byref(cfg.c()), 7, cfg.count, st.data_ptr(), _st()))
     A.check("kog_study_batch")

@@ -713,7 +713,7 @@ def test_run_batch_vs_reference_counts(cuda, ref):
                 (configs.cfg(5, count=(1 << 20) + 4099), 20),
                 # four chunks: both chunk buffers reused by the producer/consumer pipeline, a 5-matrix tail
                 (configs.cfg(5, count=3 * (1 << 22) + 5), 22),
-                # the same at the default chunk (2^23: the two-speed svd2 kernel inside the study, then a tail chunk)
+                # the same at the default chunk (one chunk: the two-speed svd2 kernel inside the study)
                 (configs.cfg(5, count=3 * (1 << 22) + 5), None),
                 # non-default Options: the general svd2 kernel inside the study
                 K.RunConfig(shape=capi.SHAPE_GEN, regime=capi.REGIME_BULLET, count=1 << 17, seed=79,
@@ -754,6 +754,33 @@ def test_run_batch_validation_and_empty(cuda):
         K.run_batch(K.RunConfig(regime=capi.REGIME_SIGMA, varsigma=0, count=10))
     with pytest.raises(ValueError):
         K.run_batch(K.RunConfig(regime=capi.REGIME_SIGMA, varsigma=5000, count=10))
+
+
+def test_study_split_equals_fused(cuda):
+    """The split study (seven instruction-cache-sized launches per chunk, the default) and the fused k_study
+    (KOG2_STUDY_SPLIT=0, read once at load: a second interpreter) give the same bytes of ErrorStats — binary64
+    and binary32, several chunks, zero patterns and non-default Options included."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys\n"
+        "from paper_2407_13116_b200 import capi, configs\n"
+        "from paper_2407_13116_b200 import kogsvd2 as K\n"
+        "capi.load().kog_study_set_chunk_log2(20)\n"
+        "cfgs = [configs.cfg(5, count=3 * (1 << 20) + 77), configs.cfg(4, count=(1 << 20) + 5), configs.cfg(2, count=1 << 18),\n"
+        "        K.RunConfig(shape=capi.SHAPE_GEN, regime=capi.REGIME_BULLET, count=1 << 17, seed=79,\n"
+        "                    options=K.Options(hypot_is_cr=False, ominus_for_d=True))]\n"
+        "for c in cfgs:\n"
+        "    s = K.StudyStats(); s.add(c, 0, c.count); print(bytes(s.read()).hex())\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for split in ("1", "0"):
+        env = dict(os.environ, KOG2_STUDY_SPLIT=split, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.split())
+    assert len(outs[0]) == 4 and outs[0] == outs[1]
 
 
 def test_study_sharding_bit_identical(cuda):

@@ -115,11 +115,16 @@ def test_studies_on_two_streams(cuda, ref):
     """Two kog_study_batch calls in flight at once on two streams (each with
     its own device ErrorStats): both equal the same studies run one at a time,
     and the smaller one equals the reference's run_batch."""
-    cfg_a = configs.cfg(5, count=2 * (1 << 23) + 4099)   # three chunks: both chunk buffers in use
+    cfg_a = configs.cfg(5, count=2 * (1 << 22) + 4099)   # three chunks of 2^22: both chunk buffers in use
     cfg_b = K.RunConfig(shape=capi.SHAPE_GEN, regime=capi.REGIME_BULLET, count=(1 << 18) + 5, seed=0x5E1)
     cfg_c = K.RunConfig(shape=capi.SHAPE_TRI, regime=capi.REGIME_BULLET, count=50000, seed=0x5E2,
                         routine=capi.ROUTINE_LASV2)
     cfgs = [cfg_a, cfg_b, cfg_c]
+    with _gen.study_chunk(22):
+        _studies_on_two_streams(ref, cfgs)
+
+
+def _studies_on_two_streams(ref, cfgs):
     serial = []
     for cfg in cfgs:
         s = K.StudyStats()
@@ -145,7 +150,7 @@ def test_studies_on_two_streams(cuda, ref):
 
 def test_study_and_svd2_share_nothing(cuda, ref):
     """A study on one stream while svd2 batches run on another."""
-    cfg = configs.cfg(5, count=(1 << 23) + 17)
+    cfg = configs.cfg(5, count=(1 << 24) + 17)  # (two chunks at the default 2^24)
     s0 = K.StudyStats()
     s0.add(cfg, 0, cfg.count)
     want_st = bytes(s0.read())
