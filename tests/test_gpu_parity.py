@@ -775,12 +775,13 @@ def test_study_split_equals_fused(cuda):
         "    s = K.StudyStats(); s.add(c, 0, c.count); print(bytes(s.read()).hex())\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for split in ("1", "0"):
-        env = dict(os.environ, KOG2_STUDY_SPLIT=split, PYTHONPATH=root)
+    # (and the pipeline's stream modes: everything on the caller's stream, one consumer stream, two)
+    for split, streams in (("1", "1"), ("0", "1"), ("1", "0"), ("1", "2")):
+        env = dict(os.environ, KOG2_STUDY_SPLIT=split, KOG2_STUDY_STREAMS=streams, PYTHONPATH=root)
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.split())
-    assert len(outs[0]) == 4 and outs[0] == outs[1]
+    assert len(outs[0]) == 4 and all(o == outs[0] for o in outs[1:])
 
 
 def test_study_sharding_bit_identical(cuda):
