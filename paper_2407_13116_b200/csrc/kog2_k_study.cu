@@ -115,15 +115,18 @@ __device__ __forceinline__ uint32_t run_one_buf(const Mat<T>& g, const SvdBuf<T>
 // fetch code (ncu r8: 22% of stall samples `no_instructions`, the GPC instruction cache at 41% of its request
 // peak with a 41% hit rate; with 20 warps per SM instead of 16 the same code ran 3x slower, 80% of samples
 // `no_instructions`).  The phased study therefore runs the body as separate kernels whose loops stay in the
-// instruction cache — the reference singular values, the reconstruction error, one orthogonality defect per
-// launch — and a last kernel that adds the singular values' errors and absorbs; the pieces go through
-// 10 x 8 B per matrix of chunk buffers.  Same operations on the same values: identical statistics.
+// instruction cache — the reference singular values in two launches (triangular factor; singular values, their
+// errors and kappa_2), the reconstruction error in two (residual norm; ratio), one orthogonality defect per
+// launch, the rare lanes off the Xf route — and a last kernel that only reads the pieces and absorbs them; the
+// pieces go through nine 8-byte and six 4-byte arrays per chunk.  Same operations on the same values: identical
+// statistics ("the split study"; profiles/r14_study_kernels.txt has the history).
 struct StudyAux {
   double *reG, *reU, *reV, *reS1, *reS2, *kh, *kl;  // kappa_2 = (ke, kh, kl)
   int32_t* ke;
   double *xh3, *xl3;   // between k_study_urv and k_study_sigma: the third intermediate (the first two in the
   int32_t *xe2, *xe3;  // result slots)
-  uint32_t* sflag;  // bit 0: the reference singular values are finite; bit 1: kappa_inf
+  uint32_t* sflag;  // between urv and sigma: ref_urv_xf's kind; then bit 0: the reference singular values are
+                    // finite, bit 1: kappa_inf, and from k_study_whole bit 2: non-finite factor, bit 3: wide exponent
   uint32_t* fin;    // g, u, v and the computed singular values are finite (with bit 0 above: metrics()'s Xf route)
   uint32_t *list, *count;  // the chunk's lanes off that route (k_study_whole's work list)
 };
