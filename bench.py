@@ -480,6 +480,9 @@ def main() -> None:
         srate = cfg5.count / dt
         sbound = fp64_ops / W_STUDY[3]
         study = {"metric": "fused study matrices/s (generate+svd2+svd2_ext+metrics+reduce)",
+                 "kernels": "per 2^24-matrix chunk: k_generate, k_svd2_lean + k_svd2_list, k_study_urv, "
+                            "k_study_sigma, k_study_recon, k_study_ratio, k_study_ortho x2, k_study_whole, "
+                            "k_study (absorb); k_study_finish once",
                  "value": srate, "unit": UNIT, "count": cfg5.count, "seconds": dt,
                  "scaling": "strong", "csv": K.csv_row(cfg5, st),
                  "allreduce": ("kog_study_allreduce (C++ ncclAllReduce MAX of the packed stats)" if nccl is not None
@@ -489,7 +492,8 @@ def main() -> None:
                               "frac": srate / sbound, "bound_rate": sbound,
                               "note": "reference-sequence FP64 ops (svd2 + svd2_ext + metrics, SURVEY.md §8(d)) "
                                       "against the in-run DFMA probe, one op per FMA; HBM is not binding "
-                                      "(generated on device, ~200 B/matrix of chunk buffers)"}}
+                                      "(generated on device, 192 B/matrix of chunk buffers, ~650 B/matrix of "
+                                      "DRAM traffic over the chunk's launches)"}}
         ss.free()
         if nccl is not None:
             nccl.close()
