@@ -143,6 +143,9 @@ __device__ __forceinline__ Mat<T> factor_of(T q11, T q12, bool neg21, bool neg22
 #ifndef KOG2_SPLIT_MINB
 #define KOG2_SPLIT_MINB 4
 #endif
+#ifndef KOG2_RATIO_MINB
+#define KOG2_RATIO_MINB 5  // (548 -> 524 us per 2^24; the other split kernels spill at 48 registers and lose)
+#endif
 #ifndef KOG2_ABSORB_MINB
 #define KOG2_ABSORB_MINB 4
 #endif
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_recon(InP<T
 }
 // ... then its root over ||G||_F
 template <class T>
-__global__ void __launch_bounds__(kThreads, KOG2_SPLIT_MINB) k_study_ratio(InP<T> in, StudyAux a, uint64_t n) {
+__global__ void __launch_bounds__(kThreads, KOG2_RATIO_MINB) k_study_ratio(InP<T> in, StudyAux a, uint64_t n) {
   for (uint64_t i = gtid(); i < n; i += gstride()) {
     const Mat<T> g = load_mat(in, i);
     const Xf sq{a.xe3[i], a.xh3[i], a.xl3[i]};
